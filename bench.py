@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- lookups/s of the B200-native XSBench / RSBench lookup (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C4|C5|C1] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step is one pass of the whole hot path (or B1-B4 for C5) over
+the rank's shard of the config's event lookups: sample -> locality sort -> search / interpolate /
+accumulate -> hash reduction, then the cross-rank int64 all-reduce of the raw hash (NCCL) when
+N > 1.  The grid build (A0) runs once before timing and is reported separately (grid_build_ms),
+like the paper's kernel-only timing.  Default workload: C3 = XSBench large,
+unionized grid, 17 M lookups (BASELINE.json configs[2], the north_star's target), strong-scaled
+over N ranks.  Every step is timed with CUDA events on the launching stream; L2 is flushed by a
+256 MiB write between steps (outside the events).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (bench, n_iso, grid_type, n_lookups, description)
+    "C1": ("xs", 68, 0, 100_000, "XSBench small 68x11303, nuclide-grid search, 100k event lookups"),
+    "C2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized grid, 17M event lookups"),
+    "C3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized grid, 17M event lookups"),
+    "C4": ("xs", 355, 2, 170_000_000, "XSBench large 355x11303, hash grid 10000 bins, 170M event lookups"),
+    "C5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, windowed multipole + Faddeeva, 10.2M lookups"),
+}
+# Per-lookup algorithmic work of the dominant kernel:
+#   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
+ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, None)}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        mx = max(float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit())
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6650.0, "src": "fallback B200_PROFILING.md"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        peaks.update(hbm_gbs=d.get("hbm_gbs", peaks["hbm_gbs"]), sm_max_mhz=d.get("sm_max_mhz", 1965.0),
+                     src="MEASURED_PEAKS.json")
+    probe = os.path.join(ROOT, "profiles", "roofline_probe.json")
+    if os.path.exists(probe):
+        d = json.load(open(probe))
+        peaks["fp64_dadd_ops_per_s"] = d.get("fp64_dadd_ops_per_s")
+        peaks["gather96_GBps"] = d.get("gather96_best_useful_GBps")
+        peaks["probe_src"] = "profiles/roofline_probe.json"
+    if not peaks.get("fp64_dadd_ops_per_s"):
+        # guide unit counts: 148 SMs x 64 FP64 lanes x 1.965 GHz (non-FMA op rate)
+        peaks["fp64_dadd_ops_per_s"] = 148 * 64 * 1.965e9
+        peaks["probe_src"] = "derived 148 SM x 64 lanes x 1965 MHz"
+    return peaks
+
+
+def cpu_baseline(cfg_name, seconds=12.0):
+    """The oracle as it stands, timed on this host's cores on a bounded sample of the workload."""
+    import oracle as O
+    bench, n_iso, gt, n, _ = CONFIGS[cfg_name]
+    threads = len(os.sched_getaffinity(0))
+    if bench == "xs":
+        o = O.XSOracle(n_iso, 11303, gt, bins=10000)
+    else:
+        o = O.RSOracle(n_iso, 1000, 100, 4)
+    k = 20_000
+    t = time.perf_counter()
+    o.lookup_batch(0, k, threads=threads)
+    dt = time.perf_counter() - t
+    k2 = int(min(n, max(k, k * seconds / max(dt, 1e-6))))
+    t = time.perf_counter()
+    o.lookup_batch(0, k2, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": k2 / dt, "unit": "lookups/s", "cores": threads, "kind": "oracle",
+            "sample": f"global lookup indices [0, {k2}) of {cfg_name} ({k2 / n:.2%} of the workload), "
+                      f"plain C oracle -O2 -ffp-contract=off, OpenMP {threads} threads, {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (the reference arm for this tier), on this host's cores."""
+    if rank != 0:
+        return
+    import oracle as O
+    cfg_name = args.config
+    bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
+    threads = len(os.sched_getaffinity(0))
+    o = O.XSOracle(n_iso, 11303, gt, bins=10000) if bench == "xs" else O.RSOracle(n_iso, 1000, 100, 4)
+    t = time.perf_counter()
+    o.lookup_batch(0, 20_000, threads=threads)
+    per = (time.perf_counter() - t) / 20_000
+    step_n = int(max(20_000, min(n, 2.0 / max(per, 1e-9))))  # ~2 s of CPU per step
+    first = 0
+    for _ in range(args.warmup):
+        o.lookup_batch(first, step_n, threads=threads)
+        first = (first + step_n) % max(1, n - step_n)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        o.lookup_batch(first, step_n, threads=threads)
+        times.append(time.perf_counter() - t)
+        first = (first + step_n) % max(1, n - step_n)
+    tot = sum(times)
+    v = step_n * args.steps / tot
+    line = {"impl": "reference", "metric": "lookups/sec", "value": v, "unit": "lookups/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
+            "config": {"workload": f"{cfg_name}: {desc}", "n_lookups": n, "step_sample": step_n},
+            "cpu_baseline": {"value": v, "unit": "lookups/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{step_n} consecutive lookups per step out of {n}"},
+            "e2e": {"value": v, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-sort", action="store_true", help="skip the A2 locality sort (unsorted gather kernel)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2306_11686_b200 as gf
+    from paper_2306_11686_b200 import build as gfbuild
+    if rank == 0 and gfbuild.needs_build():
+        gfbuild.build()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    dev = torch.device("cuda", local)
+    bench, n_iso, gt, n_total, desc = CONFIGS[args.config]
+    first, n = gf.shard_range(n_total, rank, world)
+    st = torch.cuda.current_stream()
+
+    # ---------------------------------------------------------------- A0: grid build (untimed)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    params = gf.Params.xsbench(n_iso, 11303, gt, 10000) if bench == "xs" else gf.Params.rsbench(n_iso)
+    grid = gf.Grid(params, device=dev)
+    e1.record()
+    torch.cuda.synchronize()
+    grid_ms = e0.elapsed_time(e1)
+
+    flags = 0 if args.no_sort else gf.SORT_LOCALITY
+    scratch = torch.empty(grid.scratch_bytes(n, flags), dtype=torch.uint8, device=dev)
+    vsum = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    import ctypes as C
+    L = gf.lib()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K + args.warmup)]
+
+    def step(k):
+        ev = evs[k]
+        vsum.zero_()
+        se = (C.c_void_p * 3)(ev[0].cuda_event, ev[1].cuda_event, ev[2].cuda_event)
+        gf._check(L.gf_xs_lookup_batch_ev(grid.h, first, n, gf.STARTING_SEED, flags, None,
+                                          C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                          scratch.numel(), C.c_void_p(st.cuda_stream), se))
+        if dist is not None:
+            dist.all_reduce(vsum)
+        ev[3].record()
+
+    # events must be created before use: touch them
+    for ev in evs:
+        for e in ev:
+            e.record()
+    torch.cuda.synchronize()
+    for k in range(args.warmup):
+        flush.fill_(k & 0xFF)
+        step(k)
+    torch.cuda.synchronize()
+    raws = []
+    clocks = ClockSampler(local)
+    with clocks:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        for k in range(args.warmup, args.warmup + K):
+            flush.fill_(k & 0xFF)           # L2 flush between timed steps (outside the events)
+            step(k)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    raw = int(vsum.item())
+    step_ms = [evs[k][0].elapsed_time(evs[k][3]) for k in range(args.warmup, args.warmup + K)]
+    sort_ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(args.warmup, args.warmup + K)]
+    look_ms = [evs[k][1].elapsed_time(evs[k][2]) for k in range(args.warmup, args.warmup + K)]
+    tot_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms, sum(look_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, look_tot = t.tolist()
+    else:
+        look_tot = sum(look_ms)
+    value = n_total * K / (tot_ms * 1e-3)
+
+    # ---------------------------------------------------------------- end-to-end through the public API
+    e2e = None
+    if not args.no_e2e and bench == "xs":
+        import numpy as np
+        rng = np.random.default_rng(1234 + rank)
+        P = np.array([0.139, 0.052, 0.275, 0.134, 0.154, 0.064, 0.066, 0.055, 0.008, 0.015, 0.025, 0.013])
+        Eh = torch.from_numpy(rng.random(n)).pin_memory()
+        mh = torch.from_numpy(rng.choice(12, size=n, p=P / P.sum()).astype(np.uint8)).pin_memory()
+        for _ in range(2):
+            grid.lookup_energies(Eh, mh, want_macro=True)
+        reps = 3
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r_e2e, _m = grid.lookup_energies(Eh, mh, want_macro=True)
+            if dist is not None:
+                rt = torch.tensor([r_e2e], dtype=torch.int64, device=dev)
+                dist.all_reduce(rt)
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = t.item()
+        e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 9 * n,
+               "d2h_bytes_per_step": (40 * n + 8),
+               "path": "gf_xs_lookup_energies with GF_HOST_IO: pinned host E[n] (f64) + mat[n] (u8) in, "
+                       "macro[n][5] (f64) + raw out, per rank; host-timed incl. copies and sync"}
+        del Eh, mh
+
+    if rank == 0:
+        peaks = load_peaks()
+        alg_bytes, alg_flops = ALG[args.config]
+        per_launch_lookups = n  # one lookup-kernel launch per step per rank
+        look_avg_s = look_tot / K * 1e-3
+        roof = None
+        if bench == "xs":
+            flops = alg_flops * per_launch_lookups
+            roof = {"bound": "alu", "kernel": f"xs_lookup_{'sorted' if flags else 'direct'}<grid {gt}>",
+                    "achieved": flops / look_avg_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
+                    "unit": "TFLOP/s", "traffic": None,
+                    "note": f"{alg_flops} fp64 flops/lookup (SURVEY 8(d); division counted once) x {per_launch_lookups} "
+                            f"lookups per launch / mean launch time; peak = non-FMA fp64 op rate ({peaks['probe_src']})"}
+            roof["frac"] = roof["achieved"] / roof["peak"]
+            gb = alg_bytes * per_launch_lookups / look_avg_s / 1e9
+            roof_hbm = {"bound": "hbm", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": gb / peaks["hbm_gbs"], "note": f"{alg_bytes} B/lookup random-order sector model "
+                        f"(SURVEY 8(d)); >1 means the sort removed algorithmic bytes ({peaks['src']})"}
+        else:
+            roof = {"bound": "alu", "kernel": "rs_lookup_sorted", "achieved": None, "peak": None, "unit": None,
+                    "frac": None, "traffic": None}
+            roof_hbm = None
+        cb = None
+        if not args.no_cpu_baseline and world == 1:
+            cb = cpu_baseline(args.config)
+        clk = clocks.summary()
+        line = {
+            "metric": "lookups/sec", "value": value, "unit": "lookups/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
+            "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n,
+                       "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
+                       "parallelism": f"lookup shards x{world}, grid replicated, 1 int64 NCCL all-reduce/step"},
+            "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": K * (4 if flags else 1),
+            "clocks": clk,
+            "stage_ms": {"sort": statistics.median(sort_ms), "lookup": statistics.median(look_ms),
+                         "step": statistics.median(step_ms), "grid_build": grid_ms},
+            "hash": gf.verify(raw), "raw": raw, "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

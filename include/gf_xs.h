@@ -1,0 +1,182 @@
+/*
+ * gf_xs.h -- C ABI of the B200-native XSBench / RSBench macroscopic cross-section lookup.
+ *
+ * The operation is the data-parallel loop that GPU First (arXiv 2306.11686) runs on the GPU:
+ * "two alternative methods are available to perform the cross-section lookup as part of the
+ * neutron transport simulation: event-based lookup and history-based lookup" (PAPER.md:1408,
+ * Sec. 5.3.1 "XSBench and RSBench"; Fig. 8), on XSBench
+ * v20 / RSBench v13 inputs of "two different input sizes".  The paper states no
+ * more than that; the step-by-step semantics this library implements are the readings recorded
+ * in DESIGN.md Sec. 3 (taken from SURVEY.md Sec. 8(c)).  The entry-point names follow
+ * BASELINE.json's north_star: gf_xs_grid_init, gf_xs_lookup_batch, gf_xs_verify.
+ *
+ * Conventions (all functions):
+ *   - extern "C", noexcept: nothing throws across the boundary or aborts the process.  Faults are
+ *     returned as gf_status values; gf_xs_last_error() gives a thread-local message for the last
+ *     non-OK status.
+ *   - Ownership: the CALLER owns every byte of device memory (e.g. torch.empty(..., device='cuda')).
+ *     The library never allocates device memory.  A gf_xs_grid handle holds non-owning views into
+ *     caller memory; the caller keeps that memory alive until gf_xs_grid_free().
+ *   - Asynchrony: argument validation is synchronous (GF_E_INVAL is returned before anything is
+ *     enqueued).  Device work is enqueued on `stream` (0 = legacy default stream) and the call
+ *     returns after enqueue, except where GF_HOST_IO is set (see below).  Device faults surface as
+ *     GF_E_CUDA at the next call or at the caller's synchronisation.
+ *   - Device: every call runs on the CUDA device that was current when the grid was initialised;
+ *     the library sets it for the duration of a call and restores the caller's current device.
+ *   - Threading: a grid is immutable after init.  Concurrent lookup calls on different streams are
+ *     legal if their scratch buffers and outputs do not alias.
+ *   - There is no CPU fallback: without a usable sm_100a device every compute call returns
+ *     GF_E_CUDA (or GF_E_UNSUPPORTED).
+ */
+#ifndef GF_XS_H
+#define GF_XS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_XS_ABI_VERSION 1u
+#define GF_HASH_MODULUS 999983ull /* BASELINE.json north_star: "argmax-of-5 index summed mod 999983" */
+
+typedef struct CUstream_st *gf_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    GF_OK = 0,
+    GF_E_INVAL = 1,       /* bad argument; nothing was enqueued */
+    GF_E_NOMEM = 2,       /* a caller buffer is smaller than the matching *_bytes() query */
+    GF_E_CUDA = 3,        /* CUDA runtime / launch / device fault (message has cudaGetErrorString) */
+    GF_E_UNSUPPORTED = 4, /* a valid request this build does not implement (e.g. history mode) */
+    GF_E_MISMATCH = 5     /* gf_xs_verify: hash differs from the expected value */
+} gf_status;
+
+typedef enum { GF_XSBENCH = 0, GF_RSBENCH = 1 } gf_bench;
+
+/* XSBench energy-grid acceleration: plain per-nuclide bisection, the
+ * unionized grid with its index grid, or the hash grid with `hash_bins` bins. */
+typedef enum { GF_GRID_NUCLIDE = 0, GF_GRID_UNIONIZED = 1, GF_GRID_HASH = 2 } gf_grid_type;
+
+typedef struct {
+    uint32_t abi_version;   /* must equal GF_XS_ABI_VERSION */
+    int32_t bench;          /* gf_bench */
+    int32_t n_isotopes;     /* 68 = small, 355 = large (built-in tables); any >= 1 with custom tables */
+    int64_t n_gridpoints;   /* XS: gridpoints per nuclide, 11303 in both sizes; 2 <= n <= 16384 */
+    int32_t grid_type;      /* XS: gf_grid_type */
+    int32_t hash_bins;      /* XS hash grid: bins (10000); >= 1 */
+    int32_t avg_n_poles;    /* RS: average poles per nuclide (1000); >= 1 */
+    int32_t avg_n_windows;  /* RS: average windows per nuclide (100); >= 1 */
+    int32_t numL;           /* RS: must be 4 */
+    int32_t doppler;        /* RS: must be 1 (Doppler-broadened kernel; 0 is NEXT-3, GF_E_UNSUPPORTED) */
+    uint64_t init_seed;     /* grid / data generation LCG seed (42) */
+    const int32_t *num_nucs;/* NULL = built-in Hoogenboom-Martin tables; else HOST int32[12] ...   */
+    const int32_t *mats;    /* ... and HOST int32[12 * max_num_nucs] row-major nuclide ids        */
+    int32_t max_num_nucs;   /* row length of `mats` when custom tables are given                  */
+} gf_xs_params;
+
+/* Fills *p with the defaults of BASELINE.json configs[2] (XSBench large, unionized) for
+ * bench = GF_XSBENCH, or configs[4] (RSBench large) for GF_RSBENCH.  Host-only. */
+gf_status gf_xs_default_params(int32_t bench, gf_xs_params *p);
+
+typedef struct gf_xs_grid gf_xs_grid; /* opaque; immutable after init */
+
+/* Sizes (bytes) of the caller-owned grid buffer and of the init-only scratch buffer.
+ * Host-only; no CUDA calls.  Both buffers must be device memory, 256-byte aligned. */
+gf_status gf_xs_grid_bytes(const gf_xs_params *p, size_t *grid_bytes, size_t *init_scratch_bytes);
+
+/* A0 ("data initialization is also performed on the GPU"):
+ * builds every grid array on `device` into grid_mem, asynchronously on `stream`.  The scratch
+ * buffer may be reused by the caller once the stream has passed the init work.  *out receives a
+ * host handle (free with gf_xs_grid_free). */
+gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, size_t grid_bytes, void *scratch,
+                          size_t scratch_bytes, gf_stream_t stream, gf_xs_grid **out);
+
+/* Frees the handle only; the buffers belong to the caller.  NULL is a no-op. */
+gf_status gf_xs_grid_free(gf_xs_grid *g);
+
+/* Read-only device views of the grid arrays, for tests and tools.  Layouts (all row-major):
+ *   GF_ARR_NUCLIDE_GRID  double [n_iso][n_gp][6]  (E, total, elastic, absorption, fission, nu-fission)
+ *   GF_ARR_ENERGY        double [n_iso][n_gp]     (E column, SoA copy used by the searches)
+ *   GF_ARR_UNIONIZED     double [n_iso*n_gp]      (unionized grid only)
+ *   GF_ARR_INDEX_GRID    int32  [n_iso][pitch]    nuclide-major IG, pitch = *pitch_out >= n_iso*n_gp
+ *   GF_ARR_HASH_GRID     int32  [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
+ *   GF_ARR_CONCS         double [total]           concentrations in (material, j) order
+ *   GF_ARR_MAT_NUCS      int32  [total]           nuclide ids in (material, j) order
+ *   GF_ARR_MAT_OFFSETS   int32  [13]              CSR offsets of the two arrays above
+ *   GF_ARR_THRESHOLDS    double [12]              pick_mat thresholds T[m]
+ *   GF_ARR_RS_POLES      double [total_poles][8]  EA, RT, RA, RF (re, im)         (RSBench)
+ *   GF_ARR_RS_POLE_L     int32  [total_poles]                                      (RSBench)
+ *   GF_ARR_RS_WINDOWS    double [total_windows][4] T, A, F, (int start, int end) packed  (RSBench)
+ *   GF_ARR_RS_K0RS       double [n_iso][4]                                         (RSBench)
+ *   GF_ARR_RS_POLE_OFF   int32  [n_iso+1], GF_ARR_RS_WIN_OFF int32 [n_iso+1]       (RSBench)
+ * Returns GF_E_INVAL for an array this grid does not have. */
+typedef enum {
+    GF_ARR_NUCLIDE_GRID = 0, GF_ARR_ENERGY = 1, GF_ARR_UNIONIZED = 2, GF_ARR_INDEX_GRID = 3, GF_ARR_HASH_GRID = 4,
+    GF_ARR_CONCS = 5, GF_ARR_MAT_NUCS = 6, GF_ARR_MAT_OFFSETS = 7, GF_ARR_THRESHOLDS = 8,
+    GF_ARR_RS_POLES = 9, GF_ARR_RS_POLE_L = 10, GF_ARR_RS_WINDOWS = 11, GF_ARR_RS_K0RS = 12,
+    GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14
+} gf_array;
+gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out);
+
+/* Lookup flags. */
+enum {
+    GF_SORT_LOCALITY = 1u << 0, /* A2: bin lookups by (material, energy) before the lookup kernel
+                                   (default in bench).  Results are identical either way. */
+    GF_HISTORY = 1u << 1,       /* NEXT-1 history-based mode: GF_E_UNSUPPORTED in ABI v1 */
+    GF_HOST_IO = 1u << 2        /* outputs (and, for gf_xs_lookup_energies, inputs) are HOST
+                                   pointers; the call stages them through `scratch`, copies inside
+                                   the call and synchronises `stream` before returning */
+};
+
+/* Scratch bytes a lookup call of n lookups with `flags` needs (caller allocates on the device). */
+gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes);
+
+/* A1-A6 / B1-B4: event-based lookups with GLOBAL indices [first, first+n).
+ * Lookup i samples (E, material) from the LCG stream fast_forward(starting_seed, 2i) (1070 in the
+ * benchmarks), finds each nuclide's energy interval with the grid's search, interpolates the 5
+ * (XS) micro cross sections or evaluates the windowed multipole poles (RS), accumulates them by
+ * concentration and takes v_i = 1 + argmax over the channels.
+ *   d_macro_out: NULL, or fp64 [n][5] (XS) / [n][4] (RS), row i - first, original order.
+ *   d_vsum:      uint64; the call ADDS sum(v_i) to it (caller zeroes it), so batches and shards
+ *                compose by integer addition; the hash is computed once at the end (gf_xs_verify).
+ * n must be < 2^32 per call (split larger jobs into batches).  n == 0 enqueues nothing. */
+gf_status gf_xs_lookup_batch(const gf_xs_grid *g, uint64_t first, uint64_t n, uint64_t starting_seed, uint32_t flags,
+                             double *d_macro_out, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                             gf_stream_t stream);
+
+/* Stage timing (bench / profiling): cudaEvent_t handles (as void*; any may be NULL) recorded on
+ * `stream` before the sort stage (A1-A2), between it and the lookup kernel (A3-A6), and after the
+ * lookup kernel.  Without GF_SORT_LOCALITY the first two coincide. */
+typedef struct {
+    void *before_sort;
+    void *before_lookup;
+    void *after_lookup;
+} gf_stage_events;
+
+/* gf_xs_lookup_batch with stage events; identical launches and results. */
+gf_status gf_xs_lookup_batch_ev(const gf_xs_grid *g, uint64_t first, uint64_t n, uint64_t starting_seed,
+                                uint32_t flags, double *d_macro_out, uint64_t *d_vsum, void *scratch,
+                                size_t scratch_bytes, gf_stream_t stream, const gf_stage_events *ev);
+
+/* Same lookup for CALLER-SUPPLIED particle states (a transport code's energies and materials):
+ * E[n] in [0, 1] (finite), mat[n] in 0..11.  Device pointers, or host pointers with GF_HOST_IO.
+ * macro_out [n][5|4] (may be NULL) and vsum as in gf_xs_lookup_batch. */
+gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint8_t *mat, uint64_t n, uint32_t flags,
+                                double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
+                                gf_stream_t stream);
+
+/* Host-only finalisation: *hash = raw_sum % 999983 (R-MOD: once, after all batches and shards).
+ * If expected != UINT64_MAX and *hash != expected, returns GF_E_MISMATCH (hash still written). */
+gf_status gf_xs_verify(uint64_t raw_sum, uint64_t expected, uint64_t *hash);
+
+/* Thread-local text for the last non-OK status returned on this thread ("" if none). */
+const char *gf_xs_last_error(void);
+
+/* Build identification: "gf_xs <abi> sm_100a <nvcc version>". */
+const char *gf_xs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF_XS_H */

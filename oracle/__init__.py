@@ -138,6 +138,11 @@ def argmax5_plus1(macro) -> int:
     return lib().o_argmax5_plus1(_ptr(m))
 
 
+def argmax4_plus1(macro) -> int:
+    m = np.ascontiguousarray(macro, dtype=np.float64)
+    return lib().o_argmax4_plus1(_ptr(m))
+
+
 def fast_exp(x: float) -> float:
     return lib().o_fast_exp(x)
 

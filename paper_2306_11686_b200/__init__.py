@@ -1,0 +1,243 @@
+"""paper_2306_11686_b200 -- B200-native XSBench / RSBench macroscopic cross-section lookup.
+
+Thin Python binding over the C ABI of ``include/gf_xs.h`` (``libgfxs.so``, sm_100a).  This module
+only marshals arguments: every step of the lookup (grid build, sampling, sort, search,
+interpolation, accumulation, hash) runs in the CUDA kernels behind the ABI.  PyTorch provides the
+device memory, the current stream and (for multi-GPU) the process group.  There is no CPU
+fallback: if the library cannot be loaded, or no sm_100a device is present, calls raise.
+
+The method is the lookup loop GPU First runs on the GPU (Sec. 5.3.1); the
+step-by-step readings are in DESIGN.md Sec. 3.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB as _LIB_PATH
+
+__all__ = ["Params", "Grid", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
+           "SORT_LOCALITY", "HISTORY", "HOST_IO", "HASH_MOD", "STARTING_SEED", "shard_range", "GFError"]
+
+XSBENCH, RSBENCH = 0, 1
+NUCLIDE, UNIONIZED, HASH = 0, 1, 2
+SORT_LOCALITY, HISTORY, HOST_IO = 1, 2, 4
+HASH_MOD = 999983
+STARTING_SEED = 1070
+ABI_VERSION = 1
+
+ARR = dict(nuclide_grid=0, energy=1, unionized=2, index_grid=3, hash_grid=4, concs=5, mat_nucs=6, mat_offsets=7,
+           thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14)
+
+_STATUS = {0: "GF_OK", 1: "GF_E_INVAL", 2: "GF_E_NOMEM", 3: "GF_E_CUDA", 4: "GF_E_UNSUPPORTED", 5: "GF_E_MISMATCH"}
+
+
+class GFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Params(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("bench", C.c_int32), ("n_isotopes", C.c_int32),
+                ("n_gridpoints", C.c_int64), ("grid_type", C.c_int32), ("hash_bins", C.c_int32),
+                ("avg_n_poles", C.c_int32), ("avg_n_windows", C.c_int32), ("numL", C.c_int32),
+                ("doppler", C.c_int32), ("init_seed", C.c_uint64), ("num_nucs", C.c_void_p),
+                ("mats", C.c_void_p), ("max_num_nucs", C.c_int32)]
+
+    @classmethod
+    def xsbench(cls, n_isotopes=355, n_gridpoints=11303, grid_type=UNIONIZED, hash_bins=10000, seed=42):
+        p = cls()
+        _check(lib().gf_xs_default_params(XSBENCH, C.byref(p)))
+        p.n_isotopes, p.n_gridpoints, p.grid_type, p.hash_bins, p.init_seed = (
+            n_isotopes, n_gridpoints, grid_type, hash_bins, seed)
+        return p
+
+    @classmethod
+    def rsbench(cls, n_isotopes=355, avg_n_poles=1000, avg_n_windows=100, seed=42):
+        p = cls()
+        _check(lib().gf_xs_default_params(RSBENCH, C.byref(p)))
+        p.n_isotopes, p.avg_n_poles, p.avg_n_windows, p.init_seed = n_isotopes, avg_n_poles, avg_n_windows, seed
+        return p
+
+
+_lib = None
+
+
+def lib():
+    """Load libgfxs.so.  Fails loudly: there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(nvcc, sm_100a).  There is no CPU fallback.")
+        L = C.CDLL(_LIB_PATH)
+        vp, u64, i32, sz = C.c_void_p, C.c_uint64, C.c_int32, C.c_size_t
+        P = C.POINTER
+        sig = {
+            "gf_xs_default_params": (i32, [i32, vp]),
+            "gf_xs_grid_bytes": (i32, [vp, P(sz), P(sz)]),
+            "gf_xs_grid_init": (i32, [vp, C.c_int, vp, sz, vp, sz, vp, P(vp)]),
+            "gf_xs_grid_free": (i32, [vp]),
+            "gf_xs_grid_array": (i32, [vp, i32, P(vp), P(sz), P(C.c_int64)]),
+            "gf_xs_batch_bytes": (i32, [vp, u64, C.c_uint32, P(sz)]),
+            "gf_xs_lookup_batch": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp]),
+            "gf_xs_lookup_batch_ev": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp, vp]),
+            "gf_xs_lookup_energies": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, vp, sz, vp]),
+            "gf_xs_verify": (i32, [u64, u64, P(u64)]),
+            "gf_xs_last_error": (C.c_char_p, []),
+            "gf_xs_version": (C.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise GFError(status, lib().gf_xs_last_error().decode())
+
+
+def verify(raw: int, expected: int | None = None) -> int:
+    """hash = raw % 999983 (once, after all batches and shards: R-MOD)."""
+    h = C.c_uint64()
+    st = lib().gf_xs_verify(int(raw), (1 << 64) - 1 if expected is None else int(expected), C.byref(h))
+    if st not in (0, 5):
+        _check(st)
+    if st == 5:
+        raise GFError(5, lib().gf_xs_last_error().decode())
+    return h.value
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank r of W takes the contiguous global indices [floor(r n / W), floor((r+1) n / W))."""
+    lo, hi = (rank * n) // world, ((rank + 1) * n) // world
+    return lo, hi - lo
+
+
+def _stream_ptr(torch, stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Grid:
+    """A grid built on the GPU (A0) into torch-owned device memory.
+
+    ``Grid(Params.xsbench(...))`` or ``Grid(Params.rsbench(...))``.  The buffers stay alive as
+    long as the object does; the handle is freed on ``close()`` / garbage collection.
+    """
+
+    def __init__(self, params: Params, device=None, stream=None, num_nucs=None, mats=None):
+        import numpy as np
+        import torch
+        self.torch = torch
+        self.params = params
+        if num_nucs is not None:
+            self._nn = np.ascontiguousarray(num_nucs, dtype=np.int32)
+            self._mats = np.ascontiguousarray(mats, dtype=np.int32)
+            params.num_nucs = self._nn.ctypes.data
+            params.mats = self._mats.ctypes.data
+            params.max_num_nucs = self._mats.shape[1]
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.device = dev
+        gb, sb = C.c_size_t(), C.c_size_t()
+        _check(lib().gf_xs_grid_bytes(C.byref(params), C.byref(gb), C.byref(sb)))
+        self.grid_bytes = gb.value
+        self.buf = torch.empty(gb.value, dtype=torch.uint8, device=dev)
+        scratch = torch.empty(sb.value, dtype=torch.uint8, device=dev)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            st = _stream_ptr(torch, stream)
+            _check(lib().gf_xs_grid_init(C.byref(params), dev.index, C.c_void_p(self.buf.data_ptr()), gb.value,
+                                         C.c_void_p(scratch.data_ptr()), sb.value, st, C.byref(h)))
+            (stream or torch.cuda.current_stream()).synchronize()
+        del scratch
+        self.h = h
+        self.bench = params.bench
+        self.channels = 5 if params.bench == XSBENCH else 4
+        self._scratch = None
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().gf_xs_grid_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----------------------------------------------------------------- arrays (tests / tools)
+    def array(self, name: str):
+        """Device view (torch tensor) of one grid array; see gf_array in gf_xs.h for layouts."""
+        torch = self.torch
+        p, nb, pitch = C.c_void_p(), C.c_size_t(), C.c_int64()
+        _check(lib().gf_xs_grid_array(self.h, ARR[name], C.byref(p), C.byref(nb), C.byref(pitch)))
+        off = p.value - self.buf.data_ptr()
+        raw = self.buf[off:off + nb.value]
+        dt = {"nuclide_grid": torch.float64, "energy": torch.float64, "unionized": torch.float64,
+              "index_grid": torch.int32, "hash_grid": torch.int32, "concs": torch.float64, "mat_nucs": torch.int32,
+              "mat_offsets": torch.int32, "thresholds": torch.float64, "rs_poles": torch.float64,
+              "rs_pole_l": torch.int32, "rs_windows": torch.float64, "rs_K0RS": torch.float64,
+              "rs_pole_off": torch.int32, "rs_win_off": torch.int32}[name]
+        t = raw.view(dt)
+        return t, pitch.value
+
+    # ----------------------------------------------------------------- lookups
+    def scratch_bytes(self, n: int, flags: int) -> int:
+        b = C.c_size_t()
+        _check(lib().gf_xs_batch_bytes(self.h, n, flags, C.byref(b)))
+        return b.value
+
+    def _get_scratch(self, n: int, flags: int):
+        need = self.scratch_bytes(n, flags)
+        if self._scratch is None or self._scratch.numel() < need:
+            self._scratch = self.torch.empty(need, dtype=self.torch.uint8, device=self.device)
+        return self._scratch
+
+    def lookup_batch_async(self, first: int, n: int, vsum, seed: int = STARTING_SEED, sort: bool = True,
+                           macro_out=None, stream=None):
+        """Enqueue lookups [first, first+n); ADDS sum(1+argmax) to the int64 device tensor `vsum`."""
+        flags = SORT_LOCALITY if sort else 0
+        sc = self._get_scratch(n, flags)
+        st = _stream_ptr(self.torch, stream)
+        mo = C.c_void_p(macro_out.data_ptr()) if macro_out is not None else None
+        _check(lib().gf_xs_lookup_batch(self.h, first, n, seed, flags, mo, C.c_void_p(vsum.data_ptr()),
+                                        C.c_void_p(sc.data_ptr()), sc.numel(), st))
+
+    def lookup_batch(self, first: int, n: int, seed: int = STARTING_SEED, sort: bool = True,
+                     want_macro: bool = False, stream=None):
+        """Lookups [first, first+n) -> raw sum (int), and the [n][5|4] fp64 macro xs if asked."""
+        torch = self.torch
+        vsum = torch.zeros(1, dtype=torch.int64, device=self.device)
+        macro = torch.empty((n, self.channels), dtype=torch.float64, device=self.device) if want_macro else None
+        self.lookup_batch_async(first, n, vsum, seed, sort, macro, stream)
+        raw = int(vsum.item())
+        return (raw, macro) if want_macro else raw
+
+    def lookup_energies(self, E, mat, sort: bool = True, want_macro: bool = True, stream=None):
+        """Caller-supplied states.  Device tensors -> device outputs; pinned/CPU tensors -> the call
+        stages them (GF_HOST_IO) and returns host outputs."""
+        torch = self.torch
+        n = E.numel()
+        host = not E.is_cuda
+        flags = (SORT_LOCALITY if sort else 0) | (HOST_IO if host else 0)
+        sc = self._get_scratch(n, flags)
+        st = _stream_ptr(torch, stream)
+        if host:
+            vs = C.c_uint64(0)
+            macro = torch.empty((n, self.channels), dtype=torch.float64, pin_memory=True) if want_macro else None
+            _check(lib().gf_xs_lookup_energies(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()), n, flags,
+                                               C.c_void_p(macro.data_ptr()) if want_macro else None, C.byref(vs),
+                                               C.c_void_p(sc.data_ptr()), sc.numel(), st))
+            return (vs.value, macro) if want_macro else vs.value
+        vsum = torch.zeros(1, dtype=torch.int64, device=self.device)
+        macro = torch.empty((n, self.channels), dtype=torch.float64, device=self.device) if want_macro else None
+        _check(lib().gf_xs_lookup_energies(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()), n, flags,
+                                           C.c_void_p(macro.data_ptr()) if want_macro else None,
+                                           C.c_void_p(vsum.data_ptr()), C.c_void_p(sc.data_ptr()), sc.numel(), st))
+        raw = int(vsum.item())
+        return (raw, macro) if want_macro else raw

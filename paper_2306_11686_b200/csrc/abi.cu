@@ -1,0 +1,520 @@
+// abi.cu -- the C ABI declared in include/gf_xs.h: validation, memory layout, launches.
+//
+// Host-side responsibilities only: argument checks (synchronous, before anything is enqueued),
+// carving the caller's buffers into arrays, uploading the built-in / custom
+// material tables, and enqueueing the kernels of xs_grid.cu / xs_lookup.cu / rs.cu.  No arithmetic
+// of the method runs here.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "gf_internal.cuh"
+
+using namespace gf;
+
+// ------------------------------------------------------------------------------------------ errors
+static thread_local std::string t_err;
+
+static gf_status fail(gf_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return s;
+}
+
+#define GF_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (call);                                                                   \
+    if (_e != cudaSuccess) return fail(GF_E_CUDA, "%s: %s", #call, cudaGetErrorString(_e));    \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    ok = (prev == dev) || (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    if (ok && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------------------------------------ tables
+// Hoogenboom-Martin compositions (SURVEY.md:552-558, R-MATS), typed here for the product.
+static const int32_t kFuelSmall[34] = {58, 59, 60, 61, 40, 42, 43, 44, 45, 46, 1,  2,  3,  7,  8,  9,  10,
+                                       29, 57, 47, 48, 0,  62, 15, 33, 34, 52, 53, 54, 55, 56, 18, 23, 41};
+static const int32_t kClad[5] = {63, 64, 65, 66, 67};
+static const int32_t kWater[4] = {24, 41, 4, 5};
+static const int32_t kSteel27[27] = {19, 20, 21, 22, 35, 36, 37, 38, 39, 25, 27, 28, 29, 30,
+                                     31, 32, 26, 49, 50, 51, 11, 12, 13, 14, 6,  16, 17};
+static const int32_t kWaterSteel[21] = {24, 41, 4, 5, 19, 20, 21, 22, 35, 36, 37, 38, 39, 25, 27, 28, 29, 30, 31, 32, 26};
+static const int32_t kWaterClad[9] = {24, 41, 4, 5, 63, 64, 65, 66, 67};
+
+// CSR material tables: off[13], nuc[total].
+static gf_status build_tables(const gf_xs_params *p, std::vector<int32_t> &off, std::vector<int32_t> &nuc) {
+  off.assign(kMats + 1, 0);
+  nuc.clear();
+  const int n_iso = p->n_isotopes;
+  if (!p->num_nucs) {
+    if (p->mats) return fail(GF_E_INVAL, "mats given without num_nucs");
+    if (n_iso != 68 && n_iso != 355)
+      return fail(GF_E_INVAL, "built-in material tables exist for n_isotopes 68 or 355 (got %d)", n_iso);
+    auto add = [&](const int32_t *a, int k) { nuc.insert(nuc.end(), a, a + k); };
+    add(kFuelSmall, 34);
+    if (n_iso == 355)
+      for (int i = 68; i < 355; i++) nuc.push_back(i);
+    off[1] = (int)nuc.size();
+    add(kClad, 5); off[2] = (int)nuc.size();
+    add(kWater, 4); off[3] = (int)nuc.size();
+    add(kWater, 4); off[4] = (int)nuc.size();
+    add(kSteel27, 27); off[5] = (int)nuc.size();
+    for (int m = 5; m <= 9; m++) { add(kWaterSteel, 21); off[m + 1] = (int)nuc.size(); }
+    for (int m = 10; m <= 11; m++) { add(kWaterClad, 9); off[m + 1] = (int)nuc.size(); }
+    return GF_OK;
+  }
+  if (!p->mats || p->max_num_nucs < 1) return fail(GF_E_INVAL, "custom tables need mats and max_num_nucs >= 1");
+  for (int m = 0; m < kMats; m++) {
+    int k = p->num_nucs[m];
+    if (k < 0 || k > p->max_num_nucs) return fail(GF_E_INVAL, "num_nucs[%d] = %d outside [0, max_num_nucs]", m, k);
+    for (int j = 0; j < k; j++) {
+      int v = p->mats[(size_t)m * p->max_num_nucs + j];
+      if (v < 0 || v >= n_iso) return fail(GF_E_INVAL, "mats[%d][%d] = %d is not a nuclide id", m, j, v);
+      nuc.push_back(v);
+    }
+    off[m + 1] = (int)nuc.size();
+  }
+  return GF_OK;
+}
+
+// ------------------------------------------------------------------------------------------ layout
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  // XS
+  size_t G, Ed, U, IG, HG;
+  long long ig_pitch;
+  int hg_pitch;
+  // RS
+  size_t pole, pole_l, win, K0RS, poff, woff;
+  // both
+  size_t thr, moff, mnuc, mconc;
+  size_t total_bytes, scratch_bytes;
+};
+
+static gf_status validate(const gf_xs_params *p) {
+  if (!p) return fail(GF_E_INVAL, "params is NULL");
+  if (p->abi_version != GF_XS_ABI_VERSION)
+    return fail(GF_E_INVAL, "abi_version %u != %u", p->abi_version, GF_XS_ABI_VERSION);
+  if (p->bench != GF_XSBENCH && p->bench != GF_RSBENCH) return fail(GF_E_INVAL, "bench %d", p->bench);
+  if (p->n_isotopes < 1) return fail(GF_E_INVAL, "n_isotopes %d < 1", p->n_isotopes);
+  if (p->bench == GF_XSBENCH) {
+    if (p->n_gridpoints < 2) return fail(GF_E_INVAL, "n_gridpoints %lld < 2", (long long)p->n_gridpoints);
+    if (p->n_gridpoints > kMaxSortGp)
+      return fail(GF_E_UNSUPPORTED, "n_gridpoints %lld > %d (in-SMEM grid sort limit; XL grids are NEXT-2)",
+                  (long long)p->n_gridpoints, kMaxSortGp);
+    if (p->grid_type < 0 || p->grid_type > 2) return fail(GF_E_INVAL, "grid_type %d", p->grid_type);
+    if (p->grid_type == GF_GRID_HASH && p->hash_bins < 1) return fail(GF_E_INVAL, "hash_bins %d < 1", p->hash_bins);
+    if ((long long)p->n_isotopes * p->n_gridpoints >= (1ll << 31))
+      return fail(GF_E_UNSUPPORTED, "n_isotopes * n_gridpoints >= 2^31");
+  } else {
+    if (p->numL != 4) return fail(GF_E_INVAL, "numL must be 4 (got %d)", p->numL);
+    if (p->doppler != 1) return fail(GF_E_UNSUPPORTED, "doppler = %d: only the Doppler kernel is built (0 is NEXT-3)", p->doppler);
+    if (p->avg_n_poles < 1 || p->avg_n_windows < 1) return fail(GF_E_INVAL, "avg_n_poles / avg_n_windows must be >= 1");
+    if ((long long)p->avg_n_poles * p->n_isotopes >= (1ll << 28)) return fail(GF_E_UNSUPPORTED, "too many poles");
+  }
+  return GF_OK;
+}
+
+static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
+  memset(&L, 0, sizeof L);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  if (p->bench == GF_XSBENCH) {
+    const size_t npts = (size_t)p->n_isotopes * (size_t)p->n_gridpoints;
+    L.G = take(npts * 48);
+    L.Ed = take(npts * 8);
+    if (p->grid_type == GF_GRID_UNIONIZED) {
+      L.ig_pitch = (long long)((npts + 31) & ~size_t(31));
+      L.U = take(npts * 8);
+      L.IG = take((size_t)p->n_isotopes * (size_t)L.ig_pitch * 4);
+      L.scratch_bytes = al(npts * 8);
+    } else {
+      L.scratch_bytes = 256;
+    }
+    if (p->grid_type == GF_GRID_HASH) {
+      L.hg_pitch = (p->hash_bins + 31) & ~31;
+      L.HG = take((size_t)p->n_isotopes * (size_t)L.hg_pitch * 4);
+    }
+  } else {
+    const size_t n = (size_t)p->n_isotopes;
+    const size_t tp = (size_t)p->avg_n_poles * n, tw = (size_t)p->avg_n_windows * n;
+    L.pole = take(tp * 64);
+    L.pole_l = take(tp * 4);
+    L.win = take(tw * 32);
+    L.K0RS = take(n * 4 * 8);
+    L.poff = take((n + 1) * 4);
+    L.woff = take((n + 1) * 4);
+    L.scratch_bytes = al(2 * n * 4);
+  }
+  L.thr = take(16 * 8);
+  L.moff = take(16 * 4);
+  L.mnuc = take((size_t)(total > 0 ? total : 1) * 4);
+  L.mconc = take((size_t)(total > 0 ? total : 1) * 8);
+  L.total_bytes = o;
+  return GF_OK;
+}
+
+// ------------------------------------------------------------------------------------------ handle
+struct ArrView {
+  const void *ptr = nullptr;
+  size_t bytes = 0;
+  int64_t pitch = 0;
+};
+
+struct gf_xs_grid {
+  gf_xs_params p;
+  int device = 0;
+  int total = 0;
+  XsDev xs{};
+  RsDev rs{};
+  ArrView arr[16];
+};
+
+extern "C" {
+
+const char *gf_xs_last_error(void) { return t_err.c_str(); }
+
+const char *gf_xs_version(void) {
+  static char v[96];
+  snprintf(v, sizeof v, "gf_xs abi %u sm_100a nvcc %d.%d", GF_XS_ABI_VERSION, __CUDACC_VER_MAJOR__,
+           __CUDACC_VER_MINOR__);
+  return v;
+}
+
+gf_status gf_xs_default_params(int32_t bench, gf_xs_params *p) {
+  if (!p) return fail(GF_E_INVAL, "params is NULL");
+  memset(p, 0, sizeof *p);
+  p->abi_version = GF_XS_ABI_VERSION;
+  p->bench = bench;
+  p->n_isotopes = 355;
+  p->n_gridpoints = 11303;
+  p->grid_type = GF_GRID_UNIONIZED;
+  p->hash_bins = 10000;
+  p->avg_n_poles = 1000;
+  p->avg_n_windows = 100;
+  p->numL = 4;
+  p->doppler = 1;
+  p->init_seed = 42;
+  if (bench != GF_XSBENCH && bench != GF_RSBENCH) return fail(GF_E_INVAL, "bench %d", bench);
+  return GF_OK;
+}
+
+gf_status gf_xs_grid_bytes(const gf_xs_params *p, size_t *grid_bytes, size_t *init_scratch_bytes) {
+  try {
+    gf_status s = validate(p);
+    if (s != GF_OK) return s;
+    std::vector<int32_t> off, nuc;
+    if ((s = build_tables(p, off, nuc)) != GF_OK) return s;
+    if ((int)nuc.size() > kMaxTable) return fail(GF_E_UNSUPPORTED, "material tables larger than %d entries", kMaxTable);
+    Layout L;
+    plan(p, (int)nuc.size(), L);
+    if (grid_bytes) *grid_bytes = L.total_bytes;
+    if (init_scratch_bytes) *init_scratch_bytes = L.scratch_bytes;
+    return GF_OK;
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, size_t grid_bytes, void *scratch,
+                          size_t scratch_bytes, gf_stream_t stream, gf_xs_grid **out) {
+  try {
+    if (!out) return fail(GF_E_INVAL, "out is NULL");
+    *out = nullptr;
+    gf_status s = validate(p);
+    if (s != GF_OK) return s;
+    std::vector<int32_t> off, nuc;
+    if ((s = build_tables(p, off, nuc)) != GF_OK) return s;
+    const int total = (int)nuc.size();
+    if (total > kMaxTable) return fail(GF_E_UNSUPPORTED, "material tables larger than %d entries", kMaxTable);
+    Layout L;
+    plan(p, total, L);
+    if (!grid_mem || grid_bytes < L.total_bytes)
+      return fail(GF_E_NOMEM, "grid buffer %zu B < required %zu B", grid_bytes, L.total_bytes);
+    if (!scratch || scratch_bytes < L.scratch_bytes)
+      return fail(GF_E_NOMEM, "init scratch %zu B < required %zu B", scratch_bytes, L.scratch_bytes);
+    if (((uintptr_t)grid_mem & 255) || ((uintptr_t)scratch & 255))
+      return fail(GF_E_INVAL, "grid and scratch buffers must be 256-byte aligned");
+    int ndev = 0;
+    GF_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(GF_E_INVAL, "device %d of %d", device, ndev);
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(GF_E_CUDA, "cannot make device %d current", device);
+    cudaPointerAttributes pa;
+    GF_CUDA(cudaPointerGetAttributes(&pa, grid_mem));
+    if (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)
+      return fail(GF_E_INVAL, "grid_mem is not device memory");
+    int major = 0, minor = 0;
+    GF_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    GF_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+      return fail(GF_E_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only", device, major, minor);
+
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char *base = static_cast<char *>(grid_mem);
+    gf_xs_grid *g = new gf_xs_grid();
+    g->p = *p;
+    g->p.num_nucs = nullptr;
+    g->p.mats = nullptr;
+    g->device = device;
+    g->total = total;
+    double *thr = reinterpret_cast<double *>(base + L.thr);
+    int32_t *moff = reinterpret_cast<int32_t *>(base + L.moff);
+    int32_t *mnuc = reinterpret_cast<int32_t *>(base + L.mnuc);
+    double *mconc = reinterpret_cast<double *>(base + L.mconc);
+    // Tables are uploaded synchronously from host vectors that die with this call.
+    cudaError_t ce = cudaMemcpyAsync(moff, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess && total)
+      ce = cudaMemcpyAsync(mnuc, nuc.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce == cudaSuccess) ce = launch_tables(nullptr, thr, st);
+    auto put = [&](int w, const void *ptr, size_t bytes, int64_t pitch) { g->arr[w] = ArrView{ptr, bytes, pitch}; };
+    put(GF_ARR_THRESHOLDS, thr, 12 * 8, 12);
+    put(GF_ARR_MAT_OFFSETS, moff, 13 * 4, 13);
+    put(GF_ARR_MAT_NUCS, mnuc, (size_t)total * 4, total);
+    put(GF_ARR_CONCS, mconc, (size_t)total * 8, total);
+    if (ce == cudaSuccess && p->bench == GF_XSBENCH) {
+      XsDev &X = g->xs;
+      X.n_iso = p->n_isotopes;
+      X.n_gp = (int)p->n_gridpoints;
+      X.grid_type = p->grid_type;
+      X.bins = p->hash_bins;
+      X.n_union = (long long)X.n_iso * X.n_gp;
+      X.ig_pitch = L.ig_pitch;
+      X.hg_pitch = L.hg_pitch;
+      X.total = total;
+      double *G = reinterpret_cast<double *>(base + L.G);
+      double *Ed = reinterpret_cast<double *>(base + L.Ed);
+      double *U = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<double *>(base + L.U) : nullptr;
+      int32_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<int32_t *>(base + L.IG) : nullptr;
+      int32_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<int32_t *>(base + L.HG) : nullptr;
+      X.G = G; X.Ed = Ed; X.U = U; X.IG = IG; X.HG = HG;
+      X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
+      const size_t npts = (size_t)X.n_union;
+      put(GF_ARR_NUCLIDE_GRID, G, npts * 48, X.n_gp);
+      put(GF_ARR_ENERGY, Ed, npts * 8, X.n_gp);
+      if (U) put(GF_ARR_UNIONIZED, U, npts * 8, (int64_t)npts);
+      if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 4, X.ig_pitch);
+      if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 4, X.hg_pitch);
+      ce = launch_xs_grid(X, G, Ed, U, IG, HG, mconc, p->init_seed, static_cast<double *>(scratch), st);
+    } else if (ce == cudaSuccess) {
+      RsDev &R = g->rs;
+      const int n = p->n_isotopes;
+      const size_t tp = (size_t)p->avg_n_poles * n, tw = (size_t)p->avg_n_windows * n;
+      R.n_nuc = n;
+      R.total = total;
+      double *pole = reinterpret_cast<double *>(base + L.pole);
+      int32_t *pole_l = reinterpret_cast<int32_t *>(base + L.pole_l);
+      double4 *win = reinterpret_cast<double4 *>(base + L.win);
+      double *K0RS = reinterpret_cast<double *>(base + L.K0RS);
+      int32_t *poff = reinterpret_cast<int32_t *>(base + L.poff);
+      int32_t *woff = reinterpret_cast<int32_t *>(base + L.woff);
+      R.pole = pole; R.pole_l = pole_l; R.win = win; R.K0RS = K0RS; R.poff = poff; R.woff = woff;
+      R.thr = thr; R.moff = moff; R.mnuc = mnuc; R.mconc = mconc;
+      put(GF_ARR_RS_POLES, pole, tp * 64, 8);
+      put(GF_ARR_RS_POLE_L, pole_l, tp * 4, 1);
+      put(GF_ARR_RS_WINDOWS, win, tw * 32, 4);
+      put(GF_ARR_RS_K0RS, K0RS, (size_t)n * 32, 4);
+      put(GF_ARR_RS_POLE_OFF, poff, (size_t)(n + 1) * 4, n + 1);
+      put(GF_ARR_RS_WIN_OFF, woff, (size_t)(n + 1) * 4, n + 1);
+      ce = launch_rs_data(R, p->avg_n_poles, p->avg_n_windows, p->init_seed, pole, pole_l, win, K0RS, poff, woff,
+                          mconc, static_cast<int32_t *>(scratch), st);
+    }
+    if (ce != cudaSuccess) {
+      delete g;
+      return fail(GF_E_CUDA, "grid init: %s", cudaGetErrorString(ce));
+    }
+    *out = g;
+    return GF_OK;
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+gf_status gf_xs_grid_free(gf_xs_grid *g) {
+  delete g;
+  return GF_OK;
+}
+
+gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out) {
+  if (!g || !ptr) return fail(GF_E_INVAL, "grid or ptr is NULL");
+  if (which < 0 || which >= 16 || !g->arr[which].ptr) return fail(GF_E_INVAL, "grid has no array %d", which);
+  *ptr = g->arr[which].ptr;
+  if (bytes) *bytes = g->arr[which].bytes;
+  if (pitch_out) *pitch_out = g->arr[which].pitch;
+  return GF_OK;
+}
+
+// ------------------------------------------------------------------------------------------ lookups
+struct BatchLayout {
+  size_t counts, cursor, mstart, Es, idx, h_macro, h_vsum, h_E, h_mat, total;
+};
+
+static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
+                       BatchLayout &B) {
+  memset(&B, 0, sizeof B);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
+  if (flags & GF_SORT_LOCALITY) {
+    B.counts = take(sizeof(uint32_t) * kBins);
+    B.cursor = take(sizeof(uint32_t) * kBins);
+    B.mstart = take(sizeof(uint32_t) * 16);
+    B.Es = take(sizeof(double) * n);
+    B.idx = take(sizeof(uint32_t) * n);
+  }
+  if (flags & GF_HOST_IO) {
+    if (want_macro) B.h_macro = take(sizeof(double) * ch * n);
+    B.h_vsum = take(sizeof(uint64_t));
+    if (energies) {
+      B.h_E = take(sizeof(double) * n);
+      B.h_mat = take(n);
+    }
+  }
+  B.total = o > 0 ? o : 256;
+}
+
+gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes) {
+  if (!g || !scratch_bytes) return fail(GF_E_INVAL, "grid or scratch_bytes is NULL");
+  BatchLayout B;
+  plan_batch(g, n_lookups, flags, true, true, B);  // upper bound over the optional parts
+  *scratch_bytes = B.total;
+  return GF_OK;
+}
+
+static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uint64_t seed, const double *E,
+                            const uint8_t *mat, uint32_t flags, double *macro_out, uint64_t *vsum, void *scratch,
+                            size_t scratch_bytes, gf_stream_t stream, const gf_stage_events *ev = nullptr) {
+  if (!g) return fail(GF_E_INVAL, "grid is NULL");
+  if (!vsum) return fail(GF_E_INVAL, "vsum is NULL");
+  if (flags & GF_HISTORY) return fail(GF_E_UNSUPPORTED, "history-based mode is NEXT-1 (not built in ABI v1)");
+  if (flags & ~(uint32_t)(GF_SORT_LOCALITY | GF_HISTORY | GF_HOST_IO)) return fail(GF_E_INVAL, "unknown flags 0x%x", flags);
+  if (n >= (1ull << 32)) return fail(GF_E_INVAL, "n = %llu >= 2^32: split the job into batches", (unsigned long long)n);
+  const bool energies = E != nullptr;
+  if (energies && !mat) return fail(GF_E_INVAL, "mat is NULL");
+  const bool host_io = (flags & GF_HOST_IO) != 0;
+  BatchLayout B;
+  plan_batch(g, n, flags, macro_out != nullptr, energies, B);
+  if (n && (!scratch || scratch_bytes < B.total))
+    return fail(GF_E_NOMEM, "scratch %zu B < required %zu B", scratch_bytes, B.total);
+  if (n && ((uintptr_t)scratch & 255)) return fail(GF_E_INVAL, "scratch must be 256-byte aligned");
+  if (n == 0) return GF_OK;
+  DeviceGuard dg(g->device);
+  if (!dg.ok) return fail(GF_E_CUDA, "cannot make device %d current", g->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char *sc = static_cast<char *>(scratch);
+  const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
+
+  const double *dE = E;
+  const uint8_t *dmat = mat;
+  double *dmacro = macro_out;
+  unsigned long long *dvsum = reinterpret_cast<unsigned long long *>(vsum);
+  if (host_io) {
+    dvsum = reinterpret_cast<unsigned long long *>(sc + B.h_vsum);
+    GF_CUDA(cudaMemsetAsync(dvsum, 0, 8, st));
+    if (macro_out) dmacro = reinterpret_cast<double *>(sc + B.h_macro);
+    if (energies) {
+      GF_CUDA(cudaMemcpyAsync(sc + B.h_E, E, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      GF_CUDA(cudaMemcpyAsync(sc + B.h_mat, mat, n, cudaMemcpyHostToDevice, st));
+      dE = reinterpret_cast<const double *>(sc + B.h_E);
+      dmat = reinterpret_cast<const uint8_t *>(sc + B.h_mat);
+    }
+  }
+  SortScratch S{};
+  const bool sort = (flags & GF_SORT_LOCALITY) != 0;
+  if (sort) {
+    S.counts = reinterpret_cast<uint32_t *>(sc + B.counts);
+    S.cursor = reinterpret_cast<uint32_t *>(sc + B.cursor);
+    S.mstart = reinterpret_cast<uint32_t *>(sc + B.mstart);
+    S.Es = reinterpret_cast<double *>(sc + B.Es);
+    S.idx = reinterpret_cast<uint32_t *>(sc + B.idx);
+  }
+  cudaEvent_t ev_mid = ev ? static_cast<cudaEvent_t>(ev->before_lookup) : nullptr;
+  if (ev && ev->before_sort) GF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev->before_sort), st));
+  cudaError_t ce = g->p.bench == GF_XSBENCH
+                       ? launch_xs_lookup(g->xs, first, (uint32_t)n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid)
+                       : launch_rs_lookup(g->rs, first, (uint32_t)n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid);
+  if (ce != cudaSuccess) return fail(GF_E_CUDA, "lookup launch: %s", cudaGetErrorString(ce));
+  if (ev && ev->after_lookup) GF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev->after_lookup), st));
+  if (host_io) {
+    uint64_t add = 0;
+    if (macro_out)
+      GF_CUDA(cudaMemcpyAsync(macro_out, dmacro, sizeof(double) * ch * n, cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    *vsum += add;
+  }
+  return GF_OK;
+}
+
+gf_status gf_xs_lookup_batch(const gf_xs_grid *g, uint64_t first, uint64_t n, uint64_t starting_seed, uint32_t flags,
+                             double *d_macro_out, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                             gf_stream_t stream) {
+  try {
+    return run_lookup(g, first, n, starting_seed, nullptr, nullptr, flags, d_macro_out, d_vsum, scratch,
+                      scratch_bytes, stream);
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+gf_status gf_xs_lookup_batch_ev(const gf_xs_grid *g, uint64_t first, uint64_t n, uint64_t starting_seed,
+                                uint32_t flags, double *d_macro_out, uint64_t *d_vsum, void *scratch,
+                                size_t scratch_bytes, gf_stream_t stream, const gf_stage_events *ev) {
+  try {
+    return run_lookup(g, first, n, starting_seed, nullptr, nullptr, flags, d_macro_out, d_vsum, scratch,
+                      scratch_bytes, stream, ev);
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint8_t *mat, uint64_t n, uint32_t flags,
+                                double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
+                                gf_stream_t stream) {
+  try {
+    if (!E && n) return fail(GF_E_INVAL, "E is NULL");
+    static const double kDummy = 0.0;
+    static const uint8_t kDummyMat = 0;
+    return run_lookup(g, 0, n, 0, E ? E : &kDummy, mat ? mat : (n ? nullptr : &kDummyMat), flags, macro_out, vsum,
+                      scratch, scratch_bytes, stream);
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+gf_status gf_xs_verify(uint64_t raw_sum, uint64_t expected, uint64_t *hash) {
+  if (!hash) return fail(GF_E_INVAL, "hash is NULL");
+  *hash = raw_sum % GF_HASH_MODULUS;
+  if (expected != UINT64_MAX && *hash != expected)
+    return fail(GF_E_MISMATCH, "hash %llu != expected %llu", (unsigned long long)*hash, (unsigned long long)expected);
+  return GF_OK;
+}
+
+}  // extern "C"

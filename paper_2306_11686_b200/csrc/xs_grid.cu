@@ -1,0 +1,231 @@
+// xs_grid.cu -- A0: device-side XSBench grid build (PAPER.md:1415
+// "data initialization is also performed on the GPU").
+//
+//   K0a+b  xs_sort_fill      one CTA per nuclide: regenerate the nuclide's energies from the LCG by
+//                            skip-ahead, bitonic-sort (E, generation index) pairs in SMEM (stable by
+//                            generation index, R-TIE-SORT), then write the 48-B records in sorted
+//                            order, regenerating each record's 6 draws from its stream position.
+//   K0c    merge_round       unionized energies U = ceil(log2 n_iso) rounds of pairwise merges of the
+//                            sorted per-nuclide runs (rank of each element in its partner run).
+//   K0d    ig_build          nuclide-major index grid IG[i][e] = clamp(#{A_i <= U[e]} - 1, 0, n_gp-2)
+//                            (R-IG closed form): one bisection per 16 entries, then a linear walk.
+//   K0e    hg_build          nuclide-major hash grid HG[i][b] = grid_search(A_i, b * (1.0/bins)).
+//   K0f    concs_fill        concentrations continue the grid stream (R-CONC).
+//   thresholds               pick_mat thresholds, summed in the stated order (R-PICK).
+#include "gf_internal.cuh"
+
+namespace gf {
+
+// Volume fractions of the 12 materials (SURVEY.md:549), typed for the product independently.
+__constant__ double c_dist[kMats] = {0.140, 0.052, 0.275, 0.134, 0.154, 0.064,
+                                     0.066, 0.055, 0.008, 0.015, 0.025, 0.013};
+
+// T[m] = dist[m] + dist[m-1] + ... + dist[1] in that order; T[0] = 0 (R-PICK: the order fixes bits).
+__global__ void thresholds_kernel(double *thr) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int m = 0; m < kMats; m++) {
+    double run = 0.0;
+    for (int j = m; j > 0; j--) run = __dadd_rn(run, c_dist[j]);
+    thr[m] = run;
+  }
+}
+
+cudaError_t launch_tables(const double *, double *thr, cudaStream_t st) {
+  thresholds_kernel<<<1, 32, 0, st>>>(thr);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------ K0a+b
+__global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, double *__restrict__ Ed, int n_gp,
+                                                     int npow, uint64_t seed) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(smem);
+  uint32_t *gen = reinterpret_cast<uint32_t *>(key + npow);
+  const int nuc = blockIdx.x;
+  const uint64_t base = 6ull * (uint64_t)nuc * (uint64_t)n_gp;  // draws before this nuclide
+
+  for (int k = threadIdx.x; k < npow; k += blockDim.x) {
+    if (k < n_gp) {
+      uint64_t s = lcg_skip(seed, base + 6ull * k);
+      double E = lcg_draw(s);
+      key[k] = (unsigned long long)__double_as_longlong(E);  // E in [0, 1]: bit order == value order
+      gen[k] = (uint32_t)k;
+    } else {
+      key[k] = ~0ull;  // padding sorts last
+      gen[k] = 0xFFFFFFFFu;
+    }
+  }
+  __syncthreads();
+
+  // Bitonic sort of (key, gen) pairs, ascending, lexicographic: equal energies keep generation order.
+  for (int size = 2; size <= npow; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (npow >> 1); t += blockDim.x) {
+        int lo = 2 * stride * (t / stride) + (t % stride);
+        int hi = lo + stride;
+        bool asc = (lo & size) == 0;
+        unsigned long long ka = key[lo], kb = key[hi];
+        uint32_t ga = gen[lo], gb = gen[hi];
+        bool a_gt_b = (ka > kb) || (ka == kb && ga > gb);
+        if (a_gt_b == asc) {
+          key[lo] = kb;
+          key[hi] = ka;
+          gen[lo] = gb;
+          gen[hi] = ga;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // Write the records in sorted order; each record's 6 draws are regenerated from its position.
+  for (int k = threadIdx.x; k < n_gp; k += blockDim.x) {
+    uint32_t g = gen[k];
+    uint64_t s = lcg_skip(seed, base + 6ull * g);
+    double v[6];
+#pragma unroll
+    for (int f = 0; f < 6; f++) v[f] = lcg_draw(s);
+    double2 *rec = reinterpret_cast<double2 *>(G + ((size_t)nuc * n_gp + k) * 6);
+    rec[0] = make_double2(v[0], v[1]);
+    rec[1] = make_double2(v[2], v[3]);
+    rec[2] = make_double2(v[4], v[5]);
+    Ed[(size_t)nuc * n_gp + k] = v[0];
+  }
+}
+
+// ------------------------------------------------------------------------------------------ K0c
+// One merge round: runs of length L (last may be shorter) are merged pairwise.  An element of a
+// left run goes before partner elements equal to it (lower bound), an element of a right run after
+// them (upper bound); the result is a permutation and U is the sorted multiset.
+__global__ void merge_round(const double *__restrict__ in, double *__restrict__ out, long long N, long long L) {
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= N) return;
+  long long run = g / L, start = run * L;
+  long long pr = run ^ 1ll, pstart = pr * L;
+  double v = in[g];
+  long long rank = 0, base = start;
+  if (pstart < N) {
+    long long plen = min(L, N - pstart);
+    const double *P = in + pstart;
+    long long lo = 0, hi = plen;
+    if (run & 1ll) {  // right run: #{P <= v}
+      while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (__ldg(P + mid) <= v) lo = mid + 1; else hi = mid;
+      }
+    } else {  // left run: #{P < v}
+      while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (__ldg(P + mid) < v) lo = mid + 1; else hi = mid;
+      }
+    }
+    rank = lo;
+    base = min(start, pstart);
+  }
+  out[base + (g - start) + rank] = v;
+}
+
+// ------------------------------------------------------------------------------------------ K0d
+// 16 consecutive entries per thread: a bisection for the first, then a monotone walk (U is sorted,
+// so #{A <= U[e]} is non-decreasing in e).  Rows are 128-B aligned (pitch % 32 == 0): int4 stores.
+__global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, const double *__restrict__ U,
+                                                int32_t *__restrict__ IG, int n_gp, long long n_union,
+                                                long long pitch) {
+  const int nuc = blockIdx.y;
+  long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  if (e0 >= pitch) return;
+  const double *A = Ed + (size_t)nuc * n_gp;
+  int out[16];
+  long long eq = min(e0, n_union - 1);
+  double q = __ldg(U + eq);
+  int lo = 0, hi = n_gp;  // c = #{A <= q}
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(A + mid) <= q) lo = mid + 1; else hi = mid;
+  }
+  int c = lo;
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    long long e = e0 + k;
+    if (e < n_union) {
+      q = __ldg(U + e);
+      while (c < n_gp && __ldg(A + c) <= q) c++;
+    }
+    int v = c - 1;
+    v = v < 0 ? 0 : v;
+    v = v > n_gp - 2 ? n_gp - 2 : v;
+    out[k] = v;
+  }
+  int4 *dst = reinterpret_cast<int4 *>(IG + (size_t)nuc * pitch + e0);
+#pragma unroll
+  for (int k = 0; k < 4; k++) dst[k] = make_int4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+}
+
+// ------------------------------------------------------------------------------------------ K0e
+__global__ void hg_build(const double *__restrict__ Ed, int32_t *__restrict__ HG, int n_iso, int n_gp, int bins,
+                         int pitch) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n_iso * pitch) return;
+  int nuc = (int)(t / pitch), b = (int)(t % pitch);
+  int32_t v = 0;
+  if (b < bins) {
+    double du = __ddiv_rn(1.0, (double)bins);
+    double energy = __dmul_rn((double)b, du);
+    v = bisect<int>(Ed + (size_t)nuc * n_gp, energy, 0, n_gp - 1);
+  }
+  HG[(size_t)nuc * pitch + b] = v;
+}
+
+// ------------------------------------------------------------------------------------------ K0f
+__global__ void concs_fill(double *__restrict__ conc, int total, uint64_t seed, uint64_t draws_before) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= total) return;
+  uint64_t s = lcg_skip(seed, draws_before + (uint64_t)c);
+  conc[c] = lcg_draw(s);
+}
+
+static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, int32_t *IG, int32_t *HG,
+                           double *mconc, uint64_t seed, double *scratch, cudaStream_t st) {
+  cudaError_t e;
+  const long long npts = (long long)X.n_iso * X.n_gp;
+  int npow = 2;
+  while (npow < X.n_gp) npow <<= 1;
+  size_t smem = (size_t)npow * (sizeof(unsigned long long) + sizeof(uint32_t));
+  if ((e = cudaFuncSetAttribute(xs_sort_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  int threads = npow >= 1024 ? 1024 : (npow < 64 ? 64 : npow);
+  xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, X.n_gp, npow, seed);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  concs_fill<<<nblk(X.total, 256), 256, 0, st>>>(mconc, X.total, seed, 6ull * (uint64_t)npts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  if (X.grid_type == GF_GRID_UNIONIZED) {
+    int rounds = 0;
+    for (long long L = X.n_gp; L < npts; L <<= 1) rounds++;
+    if (rounds == 0) {
+      if ((e = cudaMemcpyAsync(U, Ed, sizeof(double) * npts, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    } else {
+      // ping-pong so that the last round writes U
+      const double *in = Ed;
+      long long L = X.n_gp;
+      for (int r = 0; r < rounds; r++, L <<= 1) {
+        double *out = ((rounds - r) % 2 == 1) ? U : scratch;
+        merge_round<<<nblk(npts, 256), 256, 0, st>>>(in, out, npts, L);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        in = out;
+      }
+    }
+    dim3 grid(nblk(X.ig_pitch, 256 * 16), X.n_iso);
+    ig_build<<<grid, 256, 0, st>>>(Ed, U, IG, X.n_gp, X.n_union, X.ig_pitch);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else if (X.grid_type == GF_GRID_HASH) {
+    hg_build<<<nblk((long long)X.n_iso * X.hg_pitch, 256), 256, 0, st>>>(Ed, HG, X.n_iso, X.n_gp, X.bins, X.hg_pitch);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace gf

@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C ABI) against the plain CPU oracle, element by element.
+
+XSBench: grid arrays bit-identical; per-lookup macro xs bit-identical (0 ulp; north_star allows
+1e-12 relative, R-FP makes it exact); raw hash sums equal.  RSBench: data bit-identical; macro xs
+within 1e-10 * S (R-UNIQ, S = the oracle's cancellation scale); raw hash sums equal.
+Run on a B200 via gpurun:  python -m pytest tests -m gpu -x -q
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_HASHES = os.path.join(HERE, "golden", "oracle_hashes.json")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as T
+    if not T.cuda.is_available():
+        pytest.fail("no CUDA device: the gpu tests must run on a B200 (no CPU fallback exists)")
+    return T
+
+
+@pytest.fixture(scope="module")
+def gf(torch):
+    import paper_2306_11686_b200 as G
+    from paper_2306_11686_b200 import build
+    build.build()
+    return G
+
+
+def golden():
+    return json.load(open(ORACLE_HASHES))
+
+
+def tiny_tables(n_iso):
+    rows = [[0, 2, 4], [1], [3, 0], [2], [4], [0], [4, 3, 2, 1, 0], [1, 3], [0], [1], [2], [3]]
+    nn = np.zeros(12, dtype=np.int32)
+    mats = np.zeros((12, 5), dtype=np.int32)
+    for m, r in enumerate(rows):
+        r = list(dict.fromkeys(x % n_iso for x in r))
+        nn[m] = len(r)
+        mats[m, :len(r)] = r
+    return nn, mats
+
+
+def make_pair(gf, n_iso, n_gp, grid_type, bins=10000, custom=False, seed=42):
+    if custom:
+        nn, mats = tiny_tables(n_iso)
+        o = O.XSOracle(n_iso, n_gp, grid_type, bins=bins, seed=seed, num_nucs=nn, mats=mats)
+        g = gf.Grid(gf.Params.xsbench(n_iso, n_gp, grid_type, bins, seed), num_nucs=nn, mats=mats)
+    else:
+        o = O.XSOracle(n_iso, n_gp, grid_type, bins=bins, seed=seed)
+        g = gf.Grid(gf.Params.xsbench(n_iso, n_gp, grid_type, bins, seed))
+    return o, g
+
+
+def check_arrays(o, g, full_ig=True):
+    n_iso, n_gp = o.n_iso, o.n_gp
+    G = g.array("nuclide_grid")[0].cpu().numpy().reshape(n_iso, n_gp, 6)
+    assert np.array_equal(G, o.nuclide_grid())
+    Ed = g.array("energy")[0].cpu().numpy().reshape(n_iso, n_gp)
+    assert np.array_equal(Ed, o.nuclide_grid()[:, :, 0])
+    nn, mats, concs = o.tables()
+    off = g.array("mat_offsets")[0].cpu().numpy()
+    gc = g.array("concs")[0].cpu().numpy()
+    gn = g.array("mat_nucs")[0].cpu().numpy()
+    for m in range(12):
+        assert off[m + 1] - off[m] == nn[m]
+        assert np.array_equal(gn[off[m]:off[m + 1]], mats[m, :nn[m]])
+        assert np.array_equal(gc[off[m]:off[m + 1]], concs[m, :nn[m]])
+    T = g.array("thresholds")[0].cpu().numpy()
+    assert np.array_equal(T, O.thresholds())
+    if o.grid_type == O.UNIONIZED:
+        U = g.array("unionized")[0].cpu().numpy()
+        assert np.array_equal(U, o.unionized())
+        IG, pitch = g.array("index_grid")
+        IG = IG.view(n_iso, pitch)
+        nu = n_iso * n_gp
+        if full_ig:
+            want = o.ig_rows(0, nu)                          # energy-major [e][i]
+            assert np.array_equal(IG[:, :nu].cpu().numpy().T, want)
+        else:
+            rng = np.random.default_rng(11)
+            es = rng.integers(0, nu, 4000)
+            ii = rng.integers(0, n_iso, 4000)
+            import torch
+            got = IG[torch.from_numpy(ii).to(IG.device), torch.from_numpy(es).to(IG.device)].cpu().numpy()
+            want = np.array([o.ig_entry(int(e), int(i)) for e, i in zip(es, ii)])
+            assert np.array_equal(got, want)
+    if o.grid_type == O.HASH:
+        HG, pitch = g.array("hash_grid")
+        HG = HG.view(n_iso, pitch)[:, :o.bins].cpu().numpy()
+        assert np.array_equal(HG.T, o.hash_grid())
+
+
+def check_lookups(o, g, first, n, sort=True, seed=1070):
+    raw_o, m_o = o.lookup_batch(first, n, seed=seed, want_macro=True)
+    raw_g, m_g = g.lookup_batch(first, n, seed=seed, sort=sort, want_macro=True)
+    m_g = m_g.cpu().numpy()
+    bad = np.argwhere(m_g != m_o)
+    assert bad.size == 0, f"{len(bad)} mismatching entries, first {bad[:3]}: {m_g[tuple(bad[0])]} vs {m_o[tuple(bad[0])]}"
+    assert raw_g == raw_o
+    return raw_g
+
+
+# ------------------------------------------------------------------------------------------ tiny grids
+@pytest.mark.parametrize("grid_type", [0, 1, 2])
+@pytest.mark.parametrize("n_iso,n_gp,bins", [(5, 40, 16), (3, 2, 1), (1, 7, 3), (4, 1000, 300), (5, 33, 997)])
+def test_tiny_grid_arrays_and_lookups(gf, grid_type, n_iso, n_gp, bins):
+    o, g = make_pair(gf, n_iso, n_gp, grid_type, bins=bins, custom=True)
+    check_arrays(o, g)
+    for sort in (True, False):
+        check_lookups(o, g, 0, 3001, sort=sort)  # several CTAs and a ragged tail
+    check_lookups(o, g, 12345, 517)
+
+
+def test_n_zero_and_flags(gf, torch):
+    o, g = make_pair(gf, 5, 40, 1, custom=True)
+    assert g.lookup_batch(0, 0) == 0
+    v = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(gf.GFError) as e:
+        import ctypes as C
+        sc = g._get_scratch(10, 0)
+        gf._check(gf.lib().gf_xs_lookup_batch(g.h, 0, 10, 1070, gf.HISTORY, None, C.c_void_p(v.data_ptr()),
+                                              C.c_void_p(sc.data_ptr()), sc.numel(), None))
+    assert e.value.status == 4
+    with pytest.raises(gf.GFError) as e:
+        gf._check(gf.lib().gf_xs_lookup_batch(g.h, 0, 1 << 32, 1070, 0, None, C.c_void_p(v.data_ptr()),
+                                              C.c_void_p(sc.data_ptr()), sc.numel(), None))
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------------------------------------ paper shapes
+def test_C1_small_nuclide_full(gf):
+    o, g = make_pair(gf, 68, 11303, O.NUCLIDE)
+    check_arrays(o, g)
+    raw = check_lookups(o, g, 0, 100_000)
+    assert raw == golden()["C1"]["raw"] and gf.verify(raw) == golden()["C1"]["hash"]
+    assert check_lookups(o, g, 0, 100_000, sort=False) == raw
+
+
+def test_C2_small_unionized(gf):
+    o, g = make_pair(gf, 68, 11303, O.UNIONIZED)
+    check_arrays(o, g, full_ig=True)
+    check_lookups(o, g, 0, 1_000_000)
+    check_lookups(o, g, 16_000_000, 1_000_000, sort=False)
+    raw = g.lookup_batch(0, 17_000_000)
+    assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
+
+
+def test_small_hash_grid(gf):
+    o, g = make_pair(gf, 68, 11303, O.HASH)
+    check_arrays(o, g)
+    check_lookups(o, g, 0, 300_000)
+    check_lookups(o, g, 5_000_000, 100_000, sort=False)
+
+
+def sampled_indices(n, k, seed):
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([rng.integers(0, n, k), [0, 1, n - 2, n - 1], np.arange(0, n, n // 997)]))
+    return idx
+
+
+def check_sampled_full_size(gf, torch, o, g, n, seed=7):
+    """At full size, in the bench launch configuration (sorted, one batch of n): per-lookup outputs at
+    sampled indices equal the oracle's, which computes them one by one."""
+    raw_g, m_g = g.lookup_batch(0, n, want_macro=True)
+    idx = sampled_indices(n, 3000, seed)
+    raw_o, m_o = o.lookup_indices(idx)
+    got = m_g[torch.from_numpy(idx).to(m_g.device)].cpu().numpy()
+    assert np.array_equal(got, m_o)
+    assert raw_g == g.lookup_batch(0, n)  # the output path does not change the hash
+    return raw_g
+
+
+def test_C3_large_unionized_full_size(gf, torch):
+    o, g = make_pair(gf, 355, 11303, O.UNIONIZED)
+    check_arrays(o, g, full_ig=False)
+    raw = check_sampled_full_size(gf, torch, o, g, 17_000_000)
+    gold = golden()["C3"]
+    assert raw == gold["raw"] and gf.verify(raw) == gold["hash"]
+    check_lookups(o, g, 0, 200_000)
+    check_lookups(o, g, 9_876_543, 50_000, sort=False)
+    # shard additivity: 8 virtual shards (the multi-GPU partition) sum to the full raw
+    tot = 0
+    for r in range(8):
+        lo, cnt = gf.shard_range(17_000_000, r, 8)
+        tot += g.lookup_batch(lo, cnt)
+    assert tot == raw
+
+
+def test_C4_large_hash_170M(gf, torch):
+    o, g = make_pair(gf, 355, 11303, O.HASH)
+    check_arrays(o, g)
+    check_lookups(o, g, 0, 100_000)
+    raw = 0
+    for r in range(8):  # the 8-GPU shards, each one batch (21.25 M)
+        lo, cnt = gf.shard_range(170_000_000, r, 8)
+        raw += g.lookup_batch(lo, cnt)
+    gold = golden()["C4"]
+    assert raw == gold["raw"] and gf.verify(raw) == gold["hash"]
+    idx = sampled_indices(170_000_000, 2000, 5)
+    lo, cnt = gf.shard_range(170_000_000, 7, 8)
+    raw7, m7 = g.lookup_batch(lo, cnt, want_macro=True)
+    sel = idx[(idx >= lo) & (idx < lo + cnt)]
+    _, m_o = o.lookup_indices(sel)
+    assert np.array_equal(m7[torch.from_numpy(sel - lo).to(m7.device)].cpu().numpy(), m_o)
+
+
+# ------------------------------------------------------------------------------------------ energies API
+def edge_energies(o, n_rand, seed):
+    """Seeded synthetic particle states plus the method's degenerate energies: 0, 1, exact gridpoints
+    of several nuclides, their 1-ulp neighbours, the unionized grid ends and hash-bin edges."""
+    rng = np.random.default_rng(seed)
+    G = o.nuclide_grid()
+    Es = [0.0, 1.0, math.nextafter(1.0, 0), 5e-324, 0.5]
+    for nuc in (0, 1, o.n_iso - 1):
+        for k in (0, 1, o.n_gp // 2, o.n_gp - 2, o.n_gp - 1):
+            e = float(G[nuc, k, 0])
+            Es += [e, math.nextafter(e, 0), math.nextafter(e, 2)]
+    for b in (1, 2, 77, 9999):
+        e = b * (1.0 / 10000)
+        Es += [e, math.nextafter(e, 0), math.nextafter(e, 2)]
+    Es = np.array(Es + list(rng.random(n_rand)))
+    mats = np.concatenate([np.arange(len(Es) - n_rand) % 12, rng.integers(0, 12, n_rand)]).astype(np.uint8)
+    return Es, mats
+
+
+@pytest.mark.parametrize("grid_type", [0, 1, 2])
+def test_energies_api_device_and_host(gf, torch, grid_type):
+    o, g = make_pair(gf, 68, 11303, grid_type)
+    E, mats = edge_energies(o, 5000, 3)
+    raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
+    for sort in (True, False):
+        raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=sort)
+        assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o)
+    Eh = torch.from_numpy(E).pin_memory()
+    mh = torch.from_numpy(mats).pin_memory()
+    raw_h, m_h = g.lookup_energies(Eh, mh)
+    assert raw_h == raw_o and np.array_equal(m_h.numpy(), m_o)
+
+
+# ------------------------------------------------------------------------------------------ RSBench
+def rs_pair(gf, n_nuc=355):
+    o = O.RSOracle(n_nuc, 1000, 100, 4)
+    g = gf.Grid(gf.Params.rsbench(n_nuc))
+    return o, g
+
+
+def check_rs_data(o, g):
+    d = o.data()
+    npo, nwi = o.counts()
+    poff = g.array("rs_pole_off")[0].cpu().numpy()
+    woff = g.array("rs_win_off")[0].cpu().numpy()
+    assert np.array_equal(np.diff(poff), npo) and np.array_equal(np.diff(woff), nwi)
+    assert np.array_equal(g.array("rs_poles")[0].cpu().numpy().reshape(-1, 8), d["pole"])
+    assert np.array_equal(g.array("rs_pole_l")[0].cpu().numpy(), d["pole_l"])
+    W = g.array("rs_windows")[0].cpu().numpy().reshape(-1, 4)
+    assert np.array_equal(W[:, :3], d["win"])
+    se = W[:, 3].copy().view(np.int32).reshape(-1, 2)
+    assert np.array_equal(se[:, 0], d["win_start"]) and np.array_equal(se[:, 1], d["win_end"])
+    assert np.array_equal(g.array("rs_K0RS")[0].cpu().numpy().reshape(-1, 4), d["K0RS"])
+    nn, mats = O.builtin_tables(o.n_nuc)
+    gc = g.array("concs")[0].cpu().numpy()
+    off = g.array("mat_offsets")[0].cpu().numpy()
+    for m in range(12):
+        assert np.array_equal(gc[off[m]:off[m + 1]], d["concs"][m, :nn[m]])
+
+
+def check_rs_lookups(o, g, first, n, sort=True):
+    raw_o, m_o, S = o.lookup_batch(first, n, want_macro=True)
+    raw_g, m_g = g.lookup_batch(first, n, sort=sort, want_macro=True)
+    err = np.abs(m_g.cpu().numpy() - m_o) / S[:, None]
+    assert err.max() <= 1e-10, err.max()
+    assert raw_g == raw_o
+    return err.max()
+
+
+def test_rs_large_data_and_lookups(gf, torch):
+    o, g = rs_pair(gf, 355)
+    check_rs_data(o, g)
+    check_rs_lookups(o, g, 0, 20_000)
+    check_rs_lookups(o, g, 123_457, 5_001, sort=False)
+    raw_g, m_g = g.lookup_batch(0, 10_200_000, want_macro=True)
+    gold = golden()["C5"]
+    assert raw_g == gold["raw"] and gf.verify(raw_g) == gold["hash"]
+    idx = sampled_indices(10_200_000, 1500, 9)
+    _, m_o, S = o.lookup_indices(idx)
+    got = m_g[torch.from_numpy(idx).to(m_g.device)].cpu().numpy()
+    assert (np.abs(got - m_o) / S[:, None]).max() <= 1e-10
+
+
+def test_rs_small(gf):
+    o, g = rs_pair(gf, 68)
+    check_rs_data(o, g)
+    check_rs_lookups(o, g, 0, 50_000)
+    assert g.lookup_batch(0, 1_000_000) == golden()["RS_small_1M"]["raw"]
+
+
+def test_rs_energies_api(gf, torch):
+    o, g = rs_pair(gf, 355)
+    rng = np.random.default_rng(4)
+    E = np.concatenate([[0.0, 1.0, 0.5, 1e-300, math.nextafter(1.0, 0)], rng.random(3000)])
+    mats = rng.integers(0, 12, len(E)).astype(np.uint8)
+    raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda())
+    m_g = m_g.cpu().numpy()
+    raw_o = 0
+    for t in range(len(E)):
+        m, S = o.macro(float(E[t]), int(mats[t]))
+        assert np.all(np.abs(m_g[t] - m) <= 1e-10 * max(S, 1e-300)), t
+        raw_o += O.argmax4_plus1(m)
+    assert raw_g == raw_o

@@ -1,0 +1,53 @@
+"""Runs tools/roofline_probe.cu on the GPU and writes profiles/roofline_probe.json.
+
+    python tools/roofline_probe.py            (on a B200, via gpurun)
+"""
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC = os.path.join(HERE, "roofline_probe.cu")
+LIB = os.path.join(HERE, "libroofline_probe.so")
+
+
+def build():
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", LIB, SRC])
+    return LIB
+
+
+def main(out=os.path.join(ROOT, "profiles", "roofline_probe.json")):
+    import torch  # initialises the primary context on device 0
+    torch.cuda.init()
+    L = C.CDLL(build())
+    L.probe_fp64.restype = C.c_double
+    L.probe_gather.restype = C.c_double
+    L.probe_gather.argtypes = [C.c_longlong, C.c_int, C.c_int, C.c_int]
+    L.probe_copy.restype = C.c_double
+    L.probe_copy.argtypes = [C.c_longlong]
+    res = {"when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), "gpu": torch.cuda.get_device_name(0),
+           "sms": L.probe_sm_count(), "l2_bytes": L.probe_l2_bytes(), "clock_khz_attr": L.probe_clock_khz()}
+    for name, w in (("dadd", 0), ("dmul", 1), ("ddiv", 2)):
+        best = max(L.probe_fp64(w) for _ in range(3))
+        res[f"fp64_{name}_ops_per_s"] = best
+    res["fp64_dadd_lanes_per_sm_per_clk_at_max"] = res["fp64_dadd_ops_per_s"] / (res["sms"] * 1.965e9)
+    g = {}
+    for R in (1, 2, 4, 8):
+        for tpb, bps in ((256, 4), (256, 8), (512, 4)):
+            g[f"R{R}_t{tpb}_b{bps}"] = L.probe_gather(4 << 30, R, tpb, bps)
+    res["gather96_useful_GBps"] = g
+    res["gather96_best_useful_GBps"] = max(g.values())
+    res["copy_GBps"] = max(L.probe_copy(2 << 30) for _ in range(3))
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])

@@ -99,8 +99,9 @@ gf_status gf_xs_grid_free(gf_xs_grid *g);
  *   GF_ARR_NUCLIDE_GRID  double [n_iso][n_gp][6]  (E, total, elastic, absorption, fission, nu-fission)
  *   GF_ARR_ENERGY        double [n_iso][n_gp]     (E column, SoA copy used by the searches)
  *   GF_ARR_UNIONIZED     double [n_iso*n_gp]      (unionized grid only)
- *   GF_ARR_INDEX_GRID    int32  [n_iso][pitch]    nuclide-major IG, pitch = *pitch_out >= n_iso*n_gp
- *   GF_ARR_HASH_GRID     int32  [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
+ *   GF_ARR_INDEX_GRID    uint16 [n_iso][pitch]    nuclide-major IG, pitch = *pitch_out >= n_iso*n_gp
+ *   GF_ARR_HASH_GRID     uint16 [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
+ *   GF_ARR_UNION_BINS    uint32 [16385]           #{U < b / 2^14}: top level of the unionized search
  *   GF_ARR_CONCS         double [total]           concentrations in (material, j) order
  *   GF_ARR_MAT_NUCS      int32  [total]           nuclide ids in (material, j) order
  *   GF_ARR_MAT_OFFSETS   int32  [13]              CSR offsets of the two arrays above
@@ -115,7 +116,7 @@ typedef enum {
     GF_ARR_NUCLIDE_GRID = 0, GF_ARR_ENERGY = 1, GF_ARR_UNIONIZED = 2, GF_ARR_INDEX_GRID = 3, GF_ARR_HASH_GRID = 4,
     GF_ARR_CONCS = 5, GF_ARR_MAT_NUCS = 6, GF_ARR_MAT_OFFSETS = 7, GF_ARR_THRESHOLDS = 8,
     GF_ARR_RS_POLES = 9, GF_ARR_RS_POLE_L = 10, GF_ARR_RS_WINDOWS = 11, GF_ARR_RS_K0RS = 12,
-    GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14
+    GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14, GF_ARR_UNION_BINS = 15
 } gf_array;
 gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out);
 

@@ -27,7 +27,7 @@ STARTING_SEED = 1070
 ABI_VERSION = 1
 
 ARR = dict(nuclide_grid=0, energy=1, unionized=2, index_grid=3, hash_grid=4, concs=5, mat_nucs=6, mat_offsets=7,
-           thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14)
+           thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14, union_bins=15)
 
 _STATUS = {0: "GF_OK", 1: "GF_E_INVAL", 2: "GF_E_NOMEM", 3: "GF_E_CUDA", 4: "GF_E_UNSUPPORTED", 5: "GF_E_MISMATCH"}
 
@@ -140,7 +140,12 @@ class Grid:
             params.num_nucs = self._nn.ctypes.data
             params.mats = self._mats.ctypes.data
             params.max_num_nucs = self._mats.shape[1]
-        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        if device is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        elif isinstance(device, torch.device):
+            dev = device if device.index is not None else torch.device("cuda", torch.cuda.current_device())
+        else:
+            dev = torch.device("cuda", int(device))
         self.device = dev
         gb, sb = C.c_size_t(), C.c_size_t()
         _check(lib().gf_xs_grid_bytes(C.byref(params), C.byref(gb), C.byref(sb)))
@@ -179,11 +184,13 @@ class Grid:
         off = p.value - self.buf.data_ptr()
         raw = self.buf[off:off + nb.value]
         dt = {"nuclide_grid": torch.float64, "energy": torch.float64, "unionized": torch.float64,
-              "index_grid": torch.int32, "hash_grid": torch.int32, "concs": torch.float64, "mat_nucs": torch.int32,
+              "index_grid": torch.int16, "hash_grid": torch.int16, "union_bins": torch.int32, "concs": torch.float64, "mat_nucs": torch.int32,
               "mat_offsets": torch.int32, "thresholds": torch.float64, "rs_poles": torch.float64,
               "rs_pole_l": torch.int32, "rs_windows": torch.float64, "rs_K0RS": torch.float64,
               "rs_pole_off": torch.int32, "rs_win_off": torch.int32}[name]
         t = raw.view(dt)
+        if dt == torch.int16:  # u16 interval indices (< n_gp <= 16384): non-negative as int16
+            t = t.to(torch.int32)
         return t, pitch.value
 
     # ----------------------------------------------------------------- lookups

@@ -99,7 +99,7 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   // XS
-  size_t G, Ed, U, IG, HG;
+  size_t G, Ed, U, IG, HG, ubin;
   long long ig_pitch;
   int hg_pitch;
   // RS
@@ -146,16 +146,17 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.G = take(npts * 48);
     L.Ed = take(npts * 8);
     if (p->grid_type == GF_GRID_UNIONIZED) {
-      L.ig_pitch = (long long)((npts + 31) & ~size_t(31));
+      L.ig_pitch = (long long)((npts + 63) & ~size_t(63));
       L.U = take(npts * 8);
-      L.IG = take((size_t)p->n_isotopes * (size_t)L.ig_pitch * 4);
+      L.IG = take((size_t)p->n_isotopes * (size_t)L.ig_pitch * 2);
+      L.ubin = take((size_t)(kUBins + 1) * 4);
       L.scratch_bytes = al(npts * 8);
     } else {
       L.scratch_bytes = 256;
     }
     if (p->grid_type == GF_GRID_HASH) {
-      L.hg_pitch = (p->hash_bins + 31) & ~31;
-      L.HG = take((size_t)p->n_isotopes * (size_t)L.hg_pitch * 4);
+      L.hg_pitch = (p->hash_bins + 63) & ~63;
+      L.HG = take((size_t)p->n_isotopes * (size_t)L.hg_pitch * 2);
     }
   } else {
     const size_t n = (size_t)p->n_isotopes;
@@ -189,7 +190,7 @@ struct gf_xs_grid {
   int total = 0;
   XsDev xs{};
   RsDev rs{};
-  ArrView arr[16];
+  ArrView arr[32];
 };
 
 extern "C" {
@@ -308,17 +309,19 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       double *G = reinterpret_cast<double *>(base + L.G);
       double *Ed = reinterpret_cast<double *>(base + L.Ed);
       double *U = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<double *>(base + L.U) : nullptr;
-      int32_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<int32_t *>(base + L.IG) : nullptr;
-      int32_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<int32_t *>(base + L.HG) : nullptr;
-      X.G = G; X.Ed = Ed; X.U = U; X.IG = IG; X.HG = HG;
+      uint16_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint16_t *>(base + L.IG) : nullptr;
+      uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
+      uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
+      X.G = G; X.Ed = Ed; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
       const size_t npts = (size_t)X.n_union;
       put(GF_ARR_NUCLIDE_GRID, G, npts * 48, X.n_gp);
       put(GF_ARR_ENERGY, Ed, npts * 8, X.n_gp);
       if (U) put(GF_ARR_UNIONIZED, U, npts * 8, (int64_t)npts);
-      if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 4, X.ig_pitch);
-      if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 4, X.hg_pitch);
-      ce = launch_xs_grid(X, G, Ed, U, IG, HG, mconc, p->init_seed, static_cast<double *>(scratch), st);
+      if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 2, X.ig_pitch);
+      if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 2, X.hg_pitch);
+      if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
+      ce = launch_xs_grid(X, G, Ed, U, IG, HG, ubin, mconc, p->init_seed, static_cast<double *>(scratch), st);
     } else if (ce == cudaSuccess) {
       RsDev &R = g->rs;
       const int n = p->n_isotopes;
@@ -360,7 +363,7 @@ gf_status gf_xs_grid_free(gf_xs_grid *g) {
 
 gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out) {
   if (!g || !ptr) return fail(GF_E_INVAL, "grid or ptr is NULL");
-  if (which < 0 || which >= 16 || !g->arr[which].ptr) return fail(GF_E_INVAL, "grid has no array %d", which);
+  if (which < 0 || which >= 32 || !g->arr[which].ptr) return fail(GF_E_INVAL, "grid has no array %d", which);
   *ptr = g->arr[which].ptr;
   if (bytes) *bytes = g->arr[which].bytes;
   if (pitch_out) *pitch_out = g->arr[which].pitch;
@@ -369,7 +372,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 
 // ------------------------------------------------------------------------------------------ lookups
 struct BatchLayout {
-  size_t counts, cursor, mstart, Es, idx, h_macro, h_vsum, h_E, h_mat, total;
+  size_t counts, cursor, btot, mstart, Es, idx, h_macro, h_vsum, h_E, h_mat, total;
 };
 
 static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
@@ -385,6 +388,7 @@ static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool wan
   if (flags & GF_SORT_LOCALITY) {
     B.counts = take(sizeof(uint32_t) * kBins);
     B.cursor = take(sizeof(uint32_t) * kBins);
+    B.btot = take(sizeof(uint32_t) * (kBins / kScanBlk));
     B.mstart = take(sizeof(uint32_t) * 16);
     B.Es = take(sizeof(double) * n);
     B.idx = take(sizeof(uint32_t) * n);
@@ -451,6 +455,7 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
   if (sort) {
     S.counts = reinterpret_cast<uint32_t *>(sc + B.counts);
     S.cursor = reinterpret_cast<uint32_t *>(sc + B.cursor);
+    S.btot = reinterpret_cast<uint32_t *>(sc + B.btot);
     S.mstart = reinterpret_cast<uint32_t *>(sc + B.mstart);
     S.Es = reinterpret_cast<double *>(sc + B.Es);
     S.idx = reinterpret_cast<uint32_t *>(sc + B.idx);

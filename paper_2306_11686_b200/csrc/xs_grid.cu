@@ -8,8 +8,9 @@
 //   K0c    merge_round       unionized energies U = ceil(log2 n_iso) rounds of pairwise merges of the
 //                            sorted per-nuclide runs (rank of each element in its partner run).
 //   K0d    ig_build          nuclide-major index grid IG[i][e] = clamp(#{A_i <= U[e]} - 1, 0, n_gp-2)
-//                            (R-IG closed form): one bisection per 16 entries, then a linear walk.
-//   K0e    hg_build          nuclide-major hash grid HG[i][b] = grid_search(A_i, b * (1.0/bins)).
+//                            (R-IG closed form, u16): one bisection per 32 entries, then a linear walk.
+//          ubin_build        top-level table of the two-level unionized search.
+//   K0e    hg_build          nuclide-major u16 hash grid HG[i][b] = grid_search(A_i, b * (1.0/bins)).
 //   K0f    concs_fill        concentrations continue the grid stream (R-CONC).
 //   thresholds               pick_mat thresholds, summed in the stated order (R-PICK).
 #include "gf_internal.cuh"
@@ -126,16 +127,16 @@ __global__ void merge_round(const double *__restrict__ in, double *__restrict__ 
 }
 
 // ------------------------------------------------------------------------------------------ K0d
-// 16 consecutive entries per thread: a bisection for the first, then a monotone walk (U is sorted,
-// so #{A <= U[e]} is non-decreasing in e).  Rows are 128-B aligned (pitch % 32 == 0): int4 stores.
+// 32 consecutive entries per thread: a bisection for the first, then a monotone walk (U is sorted,
+// so #{A <= U[e]} is non-decreasing in e).  u16 entries (n_gp <= 16384); rows are 128-B aligned
+// (pitch % 64 == 0): 4 x 16-B stores per thread.
 __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, const double *__restrict__ U,
-                                                int32_t *__restrict__ IG, int n_gp, long long n_union,
+                                                uint16_t *__restrict__ IG, int n_gp, long long n_union,
                                                 long long pitch) {
   const int nuc = blockIdx.y;
-  long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 32;
   if (e0 >= pitch) return;
   const double *A = Ed + (size_t)nuc * n_gp;
-  int out[16];
   long long eq = min(e0, n_union - 1);
   double q = __ldg(U + eq);
   int lo = 0, hi = n_gp;  // c = #{A <= q}
@@ -144,8 +145,9 @@ __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, c
     if (__ldg(A + mid) <= q) lo = mid + 1; else hi = mid;
   }
   int c = lo;
+  uint32_t w[16];
 #pragma unroll
-  for (int k = 0; k < 16; k++) {
+  for (int k = 0; k < 32; k++) {
     long long e = e0 + k;
     if (e < n_union) {
       q = __ldg(U + e);
@@ -154,26 +156,43 @@ __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, c
     int v = c - 1;
     v = v < 0 ? 0 : v;
     v = v > n_gp - 2 ? n_gp - 2 : v;
-    out[k] = v;
+    if (k & 1) w[k >> 1] |= (uint32_t)v << 16; else w[k >> 1] = (uint32_t)v;
   }
-  int4 *dst = reinterpret_cast<int4 *>(IG + (size_t)nuc * pitch + e0);
+  uint4 *dst = reinterpret_cast<uint4 *>(IG + (size_t)nuc * pitch + e0);
 #pragma unroll
-  for (int k = 0; k < 4; k++) dst[k] = make_int4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+  for (int k = 0; k < 4; k++) dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+}
+
+// Top-level table of the two-level unionized search: ubin[b] = #{U < b / 2^14}, ubin[2^14] = n.
+__global__ void ubin_build(const double *__restrict__ U, uint32_t *__restrict__ ubin, long long n_union) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > kUBins) return;
+  if (b == kUBins) {
+    ubin[b] = (uint32_t)n_union;
+    return;
+  }
+  const double edge = __dmul_rn((double)b, 0x1p-14);  // exact
+  long long lo = 0, hi = n_union;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (__ldg(U + mid) < edge) lo = mid + 1; else hi = mid;
+  }
+  ubin[b] = (uint32_t)lo;
 }
 
 // ------------------------------------------------------------------------------------------ K0e
-__global__ void hg_build(const double *__restrict__ Ed, int32_t *__restrict__ HG, int n_iso, int n_gp, int bins,
+__global__ void hg_build(const double *__restrict__ Ed, uint16_t *__restrict__ HG, int n_iso, int n_gp, int bins,
                          int pitch) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)n_iso * pitch) return;
   int nuc = (int)(t / pitch), b = (int)(t % pitch);
-  int32_t v = 0;
+  int v = 0;
   if (b < bins) {
     double du = __ddiv_rn(1.0, (double)bins);
     double energy = __dmul_rn((double)b, du);
     v = bisect<int>(Ed + (size_t)nuc * n_gp, energy, 0, n_gp - 1);
   }
-  HG[(size_t)nuc * pitch + b] = v;
+  HG[(size_t)nuc * pitch + b] = (uint16_t)v;
 }
 
 // ------------------------------------------------------------------------------------------ K0f
@@ -186,8 +205,8 @@ __global__ void concs_fill(double *__restrict__ conc, int total, uint64_t seed, 
 
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, int32_t *IG, int32_t *HG,
-                           double *mconc, uint64_t seed, double *scratch, cudaStream_t st) {
+cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, uint16_t *IG, uint16_t *HG,
+                           uint32_t *ubin, double *mconc, uint64_t seed, double *scratch, cudaStream_t st) {
   cudaError_t e;
   const long long npts = (long long)X.n_iso * X.n_gp;
   int npow = 2;
@@ -218,8 +237,10 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, int
         in = out;
       }
     }
-    dim3 grid(nblk(X.ig_pitch, 256 * 16), X.n_iso);
+    dim3 grid(nblk(X.ig_pitch, 256 * 32), X.n_iso);
     ig_build<<<grid, 256, 0, st>>>(Ed, U, IG, X.n_gp, X.n_union, X.ig_pitch);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ubin_build<<<nblk(kUBins + 1, 256), 256, 0, st>>>(U, ubin, X.n_union);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   } else if (X.grid_type == GF_GRID_HASH) {
     hg_build<<<nblk((long long)X.n_iso * X.hg_pitch, 256), 256, 0, st>>>(Ed, HG, X.n_iso, X.n_gp, X.bins, X.hg_pitch);

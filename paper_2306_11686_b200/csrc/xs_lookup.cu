@@ -2,13 +2,19 @@
 //
 //   A1  sampling        lookup i draws (E, material) from fast_forward(seed, 2i).  A thread handles
 //                       a run of consecutive lookups: one skip-ahead, then 2 LCG steps per lookup.
-//   A2  locality sort   counting sort by (material, energy bin): count -> scan -> scatter of E (and
-//                       the original position when per-lookup outputs are requested).  The result
-//                       is order-independent (integer hash; outputs scattered back by position).
-//   A3  energy search   unionized: bisection of U; hash: (int64)(E / (1.0/bins)); nuclide: per
+//   A2  locality sort   counting sort by (material, energy bin): count -> two-kernel scan -> scatter
+//                       of E (and the original position when per-lookup outputs are requested).
+//                       Results are order-independent (integer hash; outputs go back by position).
+//   A3  energy search   unionized: two-level search of U (the 2^14-bin table ubin narrows the
+//                       bisection to one energy bin; same result as XSBench's grid_search, which is
+//                       clamp(#{U <= E} - 1, 0, n-2)); hash: (int64)(E / (1.0/bins)); nuclide: per
 //                       nuclide bisection of the SoA energy column.
-//   A4  micro xs        per nuclide of the material, in table order: interval k, the 96-B record
-//                       pair read as 6 x 16-B vector loads, f and the 5 interpolations.
+//   A4  micro xs        per nuclide of the material, in table order: interval k (u16 index grid),
+//                       the 96-B record pair as 6 x 16-B vector loads, f and the 5 interpolations.
+//                       Software-pipelined: the record pair of nuclide j+1 and the interval of j+2
+//                       are in flight while j is computed; in the sorted kernel one thread per CTA
+//                       also issues cp.async.bulk L2 prefetches of the CTA's index-grid segments
+//                       kPrefetch nuclides ahead.
 //   A5  macro xs        macro_c += micro_c * conc_c, RN multiply then RN add, j ascending.
 //   A6  hash            v = 1 + argmax (first strict max above -1.0); warp redux -> SMEM -> one u64
 //                       atomic per CTA.
@@ -18,16 +24,11 @@
 
 namespace gf {
 
-constexpr int kRun = 8;       // consecutive lookups per thread in the sampling kernels
-constexpr int kLookupTpb = 256;
+constexpr int kRun = 8;          // consecutive lookups per thread in the sampling kernels
+constexpr int kLookupTpb = 128;  // lookup CTA size
+constexpr int kPrefetch = 16;    // nuclides of IG-segment L2 prefetch lookahead
 
 // ------------------------------------------------------------------------------------------ A1/A2
-__device__ __forceinline__ int energy_bin(double E) {
-  int b = (int)(E * (double)kNB);
-  b = b < 0 ? 0 : b;
-  return b > kNB - 1 ? kNB - 1 : b;
-}
-
 __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
@@ -56,43 +57,57 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
   }
 }
 
-// Exclusive scan of kBins counts by one CTA of 1024 threads; cursor = offsets; mstart[m] = start
-// of material m (mstart[12] = n).
-__global__ void __launch_bounds__(1024) sort_scan(const uint32_t *__restrict__ counts, uint32_t *__restrict__ cursor,
-                                                  uint32_t *__restrict__ mstart) {
-  constexpr int kPer = kBins / 1024;
-  __shared__ uint32_t warp_tot[32];
-  const int tid = threadIdx.x;
-  uint32_t sum = 0;
-  for (int k = 0; k < kPer; k++) sum += counts[tid * kPer + k];
-  // block exclusive scan of `sum`
-  uint32_t x = sum;
-  const int lane = tid & 31, wid = tid >> 5;
+// Block-exclusive scan of kScanBlk counts per CTA (coalesced); writes local offsets and the CTA total.
+__global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restrict__ counts,
+                                                       uint32_t *__restrict__ cursor, uint32_t *__restrict__ btot) {
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b = blockIdx.x * kScanBlk + tid;
+  const uint32_t c = counts[b];
+  uint32_t x = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) warp_tot[wid] = x;
+  if (lane == 31) wsum[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    uint32_t w = warp_tot[lane];
+    uint32_t w = wsum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    warp_tot[lane] = w;  // inclusive
+    wsum[lane] = w;
   }
   __syncthreads();
-  uint32_t run = x - sum + (wid > 0 ? warp_tot[wid - 1] : 0u);
-  for (int k = 0; k < kPer; k++) {
-    int b = tid * kPer + k;
-    if (b % kNB == 0) mstart[b / kNB] = run;
-    cursor[b] = run;
-    run += counts[b];
+  cursor[b] = x - c + (wid > 0 ? wsum[wid - 1] : 0u);
+  if (tid == kScanBlk - 1) btot[blockIdx.x] = wsum[31];
+}
+
+// Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n).
+__global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ cursor, const uint32_t *__restrict__ btot,
+                                                     uint32_t *__restrict__ mstart) {
+  __shared__ uint32_t s_off;
+  constexpr int nblocks = kBins / kScanBlk;
+  if (threadIdx.x < 32) {
+    uint32_t acc = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) acc += btot[i];
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if (threadIdx.x == 0) s_off = acc;
+    if (blockIdx.x == nblocks - 1) {
+      uint32_t all = 0;
+      for (int i = threadIdx.x; i < nblocks; i += 32) all += btot[i];
+      all = __reduce_add_sync(0xffffffffu, all);
+      if (threadIdx.x == 0) mstart[kMats] = all;
+    }
   }
-  if (tid == 1023) mstart[kMats] = run;
+  __syncthreads();
+  const int b = blockIdx.x * kScanBlk + threadIdx.x;
+  const uint32_t v = cursor[b] + s_off;
+  cursor[b] = v;
+  if (b % kNB == 0) mstart[b / kNB] = v;
 }
 
 __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
@@ -136,63 +151,123 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
   unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
   sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  sort_scan<<<1, 1024, 0, st>>>(S.counts, S.cursor, S.mstart);
+  scan_local<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  scan_add<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr);
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------------------------------ A3-A5
+// ------------------------------------------------------------------------------------------ A3
+// Per-lookup energy-grid index: u (unionized) or b (hash); unused for the nuclide grid.
 template <int GT>
-__device__ __forceinline__ void macro_xs(const XsDev &X, const Tables &T, double E, int mat, double m[5]) {
-  long long u = 0;
-  int b = 0;
+__device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
   if (GT == GF_GRID_UNIONIZED) {
-    u = bisect<long long>(X.U, E, 0ll, X.n_union - 1);
+    // #{U <= E} lies in [ubin[b], ubin[b+1]] for b = floor(E 2^14) (ubin[2^14] = n covers E >= 1).
+    const int b = energy_bin(E);
+    long long lo = __ldg(X.ubin + b), hi = __ldg(X.ubin + b + 1);
+    if (b == kUBins - 1) hi = X.n_union;
+    while (lo < hi) {  // c = lo + #{U[lo..hi) <= E}
+      long long mid = (lo + hi) >> 1;
+      if (__ldg(X.U + mid) <= E) lo = mid + 1; else hi = mid;
+    }
+    long long u = lo - 1;
+    u = u < 0 ? 0 : u;
+    return u > X.n_union - 2 ? X.n_union - 2 : u;
   } else if (GT == GF_GRID_HASH) {
-    double du = __ddiv_rn(1.0, (double)X.bins);
-    double q = __ddiv_rn(E, du);
-    long long bb = (long long)q;  // truncation toward zero, as the C cast
-    bb = bb > X.bins - 1 ? X.bins - 1 : bb;  // R-E1
-    bb = bb < 0 ? 0 : bb;
-    b = (int)bb;
+    const double du = __ddiv_rn(1.0, (double)X.bins);
+    long long b = (long long)__ddiv_rn(E, du);  // truncation toward zero, as the C cast
+    b = b > X.bins - 1 ? X.bins - 1 : b;          // R-E1
+    return b < 0 ? 0 : b;
   }
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------ A4/A5
+// Interval index k of nuclide `nuc` (clamped so that k + 1 is a gridpoint).
+template <int GT>
+__device__ __forceinline__ int interval(const XsDev &X, int nuc, double E, long long idx) {
+  const int n_gp = X.n_gp;
+  int k;
+  if (GT == GF_GRID_NUCLIDE) {
+    k = bisect<int>(X.Ed + (size_t)nuc * n_gp, E, 0, n_gp - 1);
+  } else if (GT == GF_GRID_UNIONIZED) {
+    k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + idx);
+  } else {
+    const double *Ed = X.Ed + (size_t)nuc * n_gp;
+    const uint16_t *hg = X.HG + (size_t)nuc * X.hg_pitch + idx;
+    const int lo_ = __ldg(hg);
+    const int hi_ = (idx == X.bins - 1) ? n_gp - 1 : (int)__ldg(hg + 1) + 1;
+    if (E <= __ldg(Ed + lo_))
+      k = 0;
+    else if (E >= __ldg(Ed + hi_))
+      k = n_gp - 1;
+    else
+      k = bisect<int>(Ed, E, lo_, hi_);
+  }
+  return k == n_gp - 1 ? k - 1 : k;
+}
+
+struct Pair {  // records k (lo) and k+1 (hi): E, total, elastic, absorption, fission, nu-fission
+  double2 l0, l1, l2, h0, h1, h2;
+};
+
+__device__ __forceinline__ Pair load_pair(const XsDev &X, int nuc, int k) {
+  const double2 *p = reinterpret_cast<const double2 *>(X.G + ((size_t)nuc * X.n_gp + k) * 6);
+  Pair P;
+  P.l0 = __ldg(p + 0);
+  P.l1 = __ldg(p + 1);
+  P.l2 = __ldg(p + 2);
+  P.h0 = __ldg(p + 3);
+  P.h1 = __ldg(p + 4);
+  P.h2 = __ldg(p + 5);
+  return P;
+}
+
+// f = (hi.E - E) / (hi.E - lo.E); x_c = hi_c - f (hi_c - lo_c); m_c += x_c * conc (all RN, no FMA).
+__device__ __forceinline__ void accumulate(const Pair &P, double E, double conc, double m[5]) {
+  const double f = __ddiv_rn(__dsub_rn(P.h0.x, E), __dsub_rn(P.h0.x, P.l0.x));
+  const double lo[5] = {P.l0.y, P.l1.x, P.l1.y, P.l2.x, P.l2.y};
+  const double hi[5] = {P.h0.y, P.h1.x, P.h1.y, P.h2.x, P.h2.y};
+#pragma unroll
+  for (int c = 0; c < 5; c++) {
+    const double x = __dsub_rn(hi[c], __dmul_rn(f, __dsub_rn(hi[c], lo[c])));
+    m[c] = __dadd_rn(m[c], __dmul_rn(x, conc));
+  }
+}
+
+// CTA-level L2 prefetch of the index-grid row segment [lo, hi) (u16 entries, 16-B aligned) of the
+// nuclide at table entry j, issued by one thread (cp.async.bulk.prefetch: no registers, no SMEM).
+struct Prefetch {
+  bool on;
+  long long lo, hi;
+};
+
+__device__ __forceinline__ void prefetch_ig(const XsDev &X, const Tables &T, const Prefetch &pf, int j) {
+  const uint16_t *a = X.IG + (size_t)T.nuc[j] * X.ig_pitch + pf.lo;
+  const uint32_t bytes = (uint32_t)((pf.hi - pf.lo) * 2);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
+
+template <int GT>
+__device__ __forceinline__ void macro_xs(const XsDev &X, const Tables &T, double E, long long idx, int mat,
+                                         double m[5], const Prefetch &pf) {
 #pragma unroll
   for (int c = 0; c < 5; c++) m[c] = 0.0;
-  const int j1 = T.off[mat + 1];
-  const int n_gp = X.n_gp;
-  for (int j = T.off[mat]; j < j1; j++) {
-    const int nuc = T.nuc[j];
+  const int j0 = T.off[mat], j1 = T.off[mat + 1];
+  if (j0 >= j1) return;
+  // pipeline: pair(j+1) and interval(j+2) are in flight while j is accumulated
+  Pair nxt = load_pair(X, T.nuc[j0], interval<GT>(X, T.nuc[j0], E, idx));
+  int k2 = (j0 + 1 < j1) ? interval<GT>(X, T.nuc[j0 + 1], E, idx) : 0;
+  for (int j = j0; j < j1; j++) {
+    const Pair cur = nxt;
     const double conc = T.conc[j];
-    const double *Ed = X.Ed + (size_t)nuc * n_gp;
-    int k;
-    if (GT == GF_GRID_NUCLIDE) {
-      k = bisect<int>(Ed, E, 0, n_gp - 1);
-    } else if (GT == GF_GRID_UNIONIZED) {
-      k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + u);
-    } else {
-      const int32_t *hg = X.HG + (size_t)nuc * X.hg_pitch + b;
-      int lo_ = __ldg(hg);
-      int hi_ = (b == X.bins - 1) ? n_gp - 1 : __ldg(hg + 1) + 1;
-      if (E <= __ldg(Ed + lo_))
-        k = 0;
-      else if (E >= __ldg(Ed + hi_))
-        k = n_gp - 1;
-      else
-        k = bisect<int>(Ed, E, lo_, hi_);
-    }
-    if (k == n_gp - 1) k = k - 1;
-    const double2 *p = reinterpret_cast<const double2 *>(X.G + ((size_t)nuc * n_gp + k) * 6);
-    const double2 l0 = __ldg(p + 0), l1 = __ldg(p + 1), l2 = __ldg(p + 2);
-    const double2 h0 = __ldg(p + 3), h1 = __ldg(p + 4), h2 = __ldg(p + 5);
-    const double f = __ddiv_rn(__dsub_rn(h0.x, E), __dsub_rn(h0.x, l0.x));
-    const double lo[5] = {l0.y, l1.x, l1.y, l2.x, l2.y};
-    const double hi[5] = {h0.y, h1.x, h1.y, h2.x, h2.y};
-#pragma unroll
-    for (int c = 0; c < 5; c++) {
-      const double x = __dsub_rn(hi[c], __dmul_rn(f, __dsub_rn(hi[c], lo[c])));
-      m[c] = __dadd_rn(m[c], __dmul_rn(x, conc));
-    }
+    if (GT == GF_GRID_UNIONIZED && pf.on && threadIdx.x == 0 && j + kPrefetch < j1)
+      prefetch_ig(X, T, pf, j + kPrefetch);
+    if (j + 1 < j1) nxt = load_pair(X, T.nuc[j + 1], k2);
+    if (j + 2 < j1) k2 = interval<GT>(X, T.nuc[j + 2], E, idx);
+    accumulate(cur, E, conc, m);
   }
 }
 
@@ -208,7 +283,7 @@ __device__ __forceinline__ uint32_t argmax5_plus1(const double m[5]) {
   return idx + 1;
 }
 
-
+// ------------------------------------------------------------------------------------------ kernels
 // Lookups in global-index order (no sort): thread t handles lookup first + t.
 template <int GT>
 __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t first, uint32_t n, uint64_t seed,
@@ -233,7 +308,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
       mat = pick_material(lcg_draw(s), T.thr);
     }
     double m[5];
-    macro_xs<GT>(X, T, E, mat, m);
+    macro_xs<GT>(X, T, E, energy_index<GT>(X, E), mat, m, Prefetch{false, 0, 0});
     v = argmax5_plus1(m);
     if (macro_out) {
 #pragma unroll
@@ -252,17 +327,43 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
                                                                double *__restrict__ macro_out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_mat[2];
+  __shared__ unsigned long long s_ulo, s_uhi;
   const Tables T = stage_tables(X.total, X.moff, X.mnuc, X.mconc, X.thr, smem);
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t p0 = blockIdx.x * blockDim.x;
+  const uint32_t p = p0 + threadIdx.x;
+  const uint32_t pc = min(p, min(n, p0 + blockDim.x) - 1);  // clamped: tail threads mirror the last lookup
+  int mat = 0;
+#pragma unroll
+  for (int m = 1; m < kMats; m++)
+    if (pc >= __ldg(mstart + m)) mat = m;
+  const double E = Es[pc];
+  const long long u = energy_index<GT>(X, E);
+  Prefetch pf{false, 0, 0};
+  if (GT == GF_GRID_UNIONIZED) {
+    // CTA-uniform material: prefetch the CTA's index-grid segments into L2 ahead of use.
+    if (threadIdx.x == 0) {
+      s_mat[0] = mat;
+      s_ulo = ~0ull;
+      s_uhi = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_mat[1] = mat;
+    atomicMin(&s_ulo, (unsigned long long)u);
+    atomicMax(&s_uhi, (unsigned long long)u);
+    __syncthreads();
+    if (s_mat[0] == s_mat[1]) {
+      pf.on = true;
+      pf.lo = (long long)(s_ulo & ~7ull);
+      pf.hi = (long long)((s_uhi + 8) & ~7ull);
+      const int j0 = T.off[mat], j1 = T.off[mat + 1];
+      if ((int)threadIdx.x < kPrefetch && j0 + (int)threadIdx.x < j1) prefetch_ig(X, T, pf, j0 + threadIdx.x);
+    }
+  }
   uint32_t v = 0;
   if (p < n) {
-    int mat = 0;
-#pragma unroll
-    for (int m = 1; m < kMats; m++)
-      if (p >= __ldg(mstart + m)) mat = m;
-    const double E = Es[p];
     double m[5];
-    macro_xs<GT>(X, T, E, mat, m);
+    macro_xs<GT>(X, T, E, u, mat, m, pf);
     v = argmax5_plus1(m);
     if (macro_out) {
       const size_t o = (size_t)idx[p] * 5;
@@ -296,9 +397,12 @@ cudaError_t launch_xs_lookup(const XsDev &X, uint64_t first, uint32_t n, uint64_
                              const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
                              unsigned long long *vsum, cudaStream_t st, cudaEvent_t ev_mid) {
   switch (X.grid_type) {
-    case GF_GRID_NUCLIDE: return launch_gt<GF_GRID_NUCLIDE>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
-    case GF_GRID_UNIONIZED: return launch_gt<GF_GRID_UNIONIZED>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
-    default: return launch_gt<GF_GRID_HASH>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+    case GF_GRID_NUCLIDE:
+      return launch_gt<GF_GRID_NUCLIDE>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+    case GF_GRID_UNIONIZED:
+      return launch_gt<GF_GRID_UNIONIZED>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+    default:
+      return launch_gt<GF_GRID_HASH>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
   }
 }
 

@@ -94,15 +94,15 @@ def test_grid_bytes_closed_form():
         total = (34 if n_iso == 68 else 321) + 5 + 4 + 4 + 27 + 5 * 21 + 2 * 9
         want = al(npts * 48) + al(npts * 8)
         if gt == gf.UNIONIZED:
-            pitch = (npts + 31) // 32 * 32
-            want += al(npts * 8) + al(n_iso * pitch * 4)
+            pitch = (npts + 63) // 64 * 64
+            want += al(npts * 8) + al(n_iso * pitch * 2) + al(16385 * 4)
         if gt == gf.HASH:
-            want += al(n_iso * 10016 * 4)
+            want += al(n_iso * 10048 * 2)
         want += al(128) + al(64) + al(total * 4) + al(total * 8)
         assert gb == want, (n_iso, gt)
-    # C3: the 355 x 4,012,565 int32 index grid (5.70 GB) dominates the 5.95 GB total
+    # C3: the 355 x 4,012,565 u16 index grid (2.85 GB) dominates the 3.10 GB total
     st, gb, _ = _bytes(gf.Params.xsbench(355, 11303, gf.UNIONIZED))
-    assert 5.94e9 < gb < 5.97e9
+    assert 3.09e9 < gb < 3.11e9
 
 
 @pytest.mark.parametrize("field,value,status", [

@@ -1,0 +1,57 @@
+"""N > 1 host path on CPU: world_size-2 gloo process group.  Each rank computes its contiguous shard
+of the lookups (here with the oracle, since there is no GPU), the raw sums are all-reduced with the
+package's reduce_raw, and the finished hash equals the single-process hash."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    import paper_2306_11686_b200 as gf
+    from paper_2306_11686_b200 import dist as gdist
+    o = O.XSOracle(68, 11303, O.NUCLIDE)
+    first, cnt = gf.shard_range(n, rank, world)
+    raw = o.lookup_batch(first, cnt, threads=1)
+    vsum = torch.tensor([raw], dtype=torch.int64)
+    gdist.reduce_raw(vsum)
+    t = gdist.max_over_ranks([float(rank + 1), 10.0 - rank], "cpu")
+    if rank == 0:
+        q.put((int(vsum.item()), gdist.finish_hash(int(vsum.item())), t))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_sharded_hash_equals_single_process(world):
+    import oracle as O
+    import paper_2306_11686_b200 as gf
+    n = 30_011  # not a multiple of the world size
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    raw, h, t = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    full = O.XSOracle(68, 11303, O.NUCLIDE).lookup_batch(0, n)
+    assert raw == full
+    assert h == gf.verify(full)
+    assert t == [2.0, 10.0]

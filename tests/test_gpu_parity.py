@@ -81,6 +81,11 @@ def check_arrays(o, g, full_ig=True):
     if o.grid_type == O.UNIONIZED:
         U = g.array("unionized")[0].cpu().numpy()
         assert np.array_equal(U, o.unionized())
+        ub = g.array("union_bins")[0].cpu().numpy().astype(np.int64)
+        edges = np.arange(16385) / 16384.0
+        want_ub = np.searchsorted(o.unionized(), edges, side="left")
+        want_ub[-1] = len(U)
+        assert np.array_equal(ub, want_ub)
         IG, pitch = g.array("index_grid")
         IG = IG.view(n_iso, pitch)
         nu = n_iso * n_gp

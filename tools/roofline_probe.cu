@@ -57,7 +57,9 @@ __global__ void k_gather(const double2 *__restrict__ buf, long long nrec, int pe
     double2 v[R][6];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      long long rec = (long long)(mix(tid * 1315423911ull + (uint64_t)(it + r) * 2654435761ull + salt) % (uint64_t)(nrec - 1));
+      // uniform record index in [0, nrec-1) by a multiply-high (no 64-bit modulo on the hot path)
+      long long rec = (long long)__umul64hi(mix(tid * 1315423911ull + (uint64_t)(it + r) * 2654435761ull + salt),
+                                            (uint64_t)(nrec - 1));
       const double2 *p = buf + rec * 3;  // 48-B record = 3 double2; a pair is 6 double2 (96 B)
 #pragma unroll
       for (int k = 0; k < 6; k++) v[r][k] = __ldg(p + k);
@@ -139,10 +141,11 @@ extern "C" double probe_gather(long long bytes, int R, int threads, int blocks_p
   cudaMalloc(&c.out, 8);
   c.threads = threads;
   c.blocks = sms * blocks_per_sm;
-  c.per = 64;
+  c.per = 128;
   c.R = R;
   c.salt = 1;
   float ms = time_it(launch_g, &c);
+  if (cudaGetLastError() != cudaSuccess) ms = -1.f;
   cudaFree((void *)c.buf);
   cudaFree(c.out);
   double gathers = (double)c.blocks * c.threads * c.per;
@@ -164,7 +167,7 @@ extern "C" double probe_copy(long long bytes) {
   if (cudaMalloc((void **)&c.a, bytes) != cudaSuccess) return -1.0;
   if (cudaMalloc((void **)&c.b, bytes) != cudaSuccess) return -1.0;
   cudaMemset((void *)c.a, 0, bytes);
-  c.blocks = sms * 4;
+  c.blocks = sms * 16;
   float ms = time_it(launch_c, &c);
   cudaFree((void *)c.a);
   cudaFree(c.b);

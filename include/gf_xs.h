@@ -102,6 +102,7 @@ gf_status gf_xs_grid_free(gf_xs_grid *g);
  *   GF_ARR_INDEX_GRID    uint16 [n_iso][pitch]    nuclide-major IG, pitch = *pitch_out >= n_iso*n_gp
  *   GF_ARR_HASH_GRID     uint16 [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
  *   GF_ARR_UNION_BINS    uint32 [16385]           #{U < b / 2^14}: top level of the unionized search
+ *   GF_ARR_RECIP_WIDTH   double [n_iso][n_gp]     RN(1 / (E[k+1] - E[k])) per interval (exact division)
  *   GF_ARR_CONCS         double [total]           concentrations in (material, j) order
  *   GF_ARR_MAT_NUCS      int32  [total]           nuclide ids in (material, j) order
  *   GF_ARR_MAT_OFFSETS   int32  [13]              CSR offsets of the two arrays above
@@ -116,7 +117,8 @@ typedef enum {
     GF_ARR_NUCLIDE_GRID = 0, GF_ARR_ENERGY = 1, GF_ARR_UNIONIZED = 2, GF_ARR_INDEX_GRID = 3, GF_ARR_HASH_GRID = 4,
     GF_ARR_CONCS = 5, GF_ARR_MAT_NUCS = 6, GF_ARR_MAT_OFFSETS = 7, GF_ARR_THRESHOLDS = 8,
     GF_ARR_RS_POLES = 9, GF_ARR_RS_POLE_L = 10, GF_ARR_RS_WINDOWS = 11, GF_ARR_RS_K0RS = 12,
-    GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14, GF_ARR_UNION_BINS = 15
+    GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14, GF_ARR_UNION_BINS = 15,
+    GF_ARR_RECIP_WIDTH = 16
 } gf_array;
 gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out);
 
@@ -166,6 +168,16 @@ gf_status gf_xs_lookup_batch_ev(const gf_xs_grid *g, uint64_t first, uint64_t n,
 gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint8_t *mat, uint64_t n, uint32_t flags,
                                 double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
                                 gf_stream_t stream);
+
+/* Grid facts: *fastdiv = 1 when the lookup kernels use the exact reciprocal division (every
+ * interval of the nuclide grid has a normal, non-zero width), 0 when they use __ddiv_rn. */
+gf_status gf_xs_grid_info(const gf_xs_grid *g, int32_t *fastdiv);
+
+/* Diagnostics: d_out[i] = the lookup kernels' reciprocal division of d_a[i] by d_b[i] (device
+ * arrays of n doubles), d_ref[i] = IEEE a / b (__ddiv_rn).  The two must agree bit for bit for
+ * |a| <= 4 and normal non-zero b.  Enqueued on `stream`. */
+gf_status gf_xs_selftest_div(const double *d_a, const double *d_b, double *d_out, double *d_ref, uint64_t n,
+                             gf_stream_t stream);
 
 /* Host-only finalisation: *hash = raw_sum % 999983 (R-MOD: once, after all batches and shards).
  * If expected != UINT64_MAX and *hash != expected, returns GF_E_MISMATCH (hash still written). */

@@ -27,7 +27,8 @@ STARTING_SEED = 1070
 ABI_VERSION = 1
 
 ARR = dict(nuclide_grid=0, energy=1, unionized=2, index_grid=3, hash_grid=4, concs=5, mat_nucs=6, mat_offsets=7,
-           thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14, union_bins=15)
+           thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14, union_bins=15,
+           recip_width=16)
 
 _STATUS = {0: "GF_OK", 1: "GF_E_INVAL", 2: "GF_E_NOMEM", 3: "GF_E_CUDA", 4: "GF_E_UNSUPPORTED", 5: "GF_E_MISMATCH"}
 
@@ -85,6 +86,8 @@ def lib():
             "gf_xs_lookup_batch_ev": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp, vp]),
             "gf_xs_lookup_energies": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_verify": (i32, [u64, u64, P(u64)]),
+            "gf_xs_grid_info": (i32, [vp, P(i32)]),
+            "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
             "gf_xs_last_error": (C.c_char_p, []),
             "gf_xs_version": (C.c_char_p, []),
         }
@@ -164,6 +167,12 @@ class Grid:
         self.channels = 5 if params.bench == XSBENCH else 4
         self._scratch = None
 
+    @property
+    def fastdiv(self) -> bool:
+        v = C.c_int32()
+        _check(lib().gf_xs_grid_info(self.h, C.byref(v)))
+        return bool(v.value)
+
     def close(self):
         if getattr(self, "h", None) and self.h.value:
             lib().gf_xs_grid_free(self.h)
@@ -184,7 +193,7 @@ class Grid:
         off = p.value - self.buf.data_ptr()
         raw = self.buf[off:off + nb.value]
         dt = {"nuclide_grid": torch.float64, "energy": torch.float64, "unionized": torch.float64,
-              "index_grid": torch.int16, "hash_grid": torch.int16, "union_bins": torch.int32, "concs": torch.float64, "mat_nucs": torch.int32,
+              "index_grid": torch.int16, "hash_grid": torch.int16, "union_bins": torch.int32, "recip_width": torch.float64, "concs": torch.float64, "mat_nucs": torch.int32,
               "mat_offsets": torch.int32, "thresholds": torch.float64, "rs_poles": torch.float64,
               "rs_pole_l": torch.int32, "rs_windows": torch.float64, "rs_K0RS": torch.float64,
               "rs_pole_off": torch.int32, "rs_win_off": torch.int32}[name]

@@ -99,7 +99,7 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   // XS
-  size_t G, Ed, U, IG, HG, ubin;
+  size_t G, Ed, Rd, flags, U, IG, HG, ubin;
   long long ig_pitch;
   int hg_pitch;
   // RS
@@ -124,6 +124,8 @@ static gf_status validate(const gf_xs_params *p) {
     if (p->grid_type == GF_GRID_HASH && p->hash_bins < 1) return fail(GF_E_INVAL, "hash_bins %d < 1", p->hash_bins);
     if ((long long)p->n_isotopes * p->n_gridpoints >= (1ll << 31))
       return fail(GF_E_UNSUPPORTED, "n_isotopes * n_gridpoints >= 2^31");
+    if ((double)p->n_isotopes * (double)(p->n_isotopes * p->n_gridpoints + 63) >= 4294967296.0)
+      return fail(GF_E_UNSUPPORTED, "index grid larger than 2^32 entries");
   } else {
     if (p->numL != 4) return fail(GF_E_INVAL, "numL must be 4 (got %d)", p->numL);
     if (p->doppler != 1) return fail(GF_E_UNSUPPORTED, "doppler = %d: only the Doppler kernel is built (0 is NEXT-3)", p->doppler);
@@ -145,6 +147,8 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     const size_t npts = (size_t)p->n_isotopes * (size_t)p->n_gridpoints;
     L.G = take(npts * 48);
     L.Ed = take(npts * 8);
+    L.Rd = take(npts * 8);
+    L.flags = take(16);
     if (p->grid_type == GF_GRID_UNIONIZED) {
       L.ig_pitch = (long long)((npts + 63) & ~size_t(63));
       L.U = take(npts * 8);
@@ -308,11 +312,13 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       X.total = total;
       double *G = reinterpret_cast<double *>(base + L.G);
       double *Ed = reinterpret_cast<double *>(base + L.Ed);
+      double *Rd = reinterpret_cast<double *>(base + L.Rd);
+      int *zero_width = reinterpret_cast<int *>(base + L.flags);
       double *U = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<double *>(base + L.U) : nullptr;
       uint16_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint16_t *>(base + L.IG) : nullptr;
       uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
       uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
-      X.G = G; X.Ed = Ed; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
+      X.G = G; X.Ed = Ed; X.Rd = Rd; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
       const size_t npts = (size_t)X.n_union;
       put(GF_ARR_NUCLIDE_GRID, G, npts * 48, X.n_gp);
@@ -321,7 +327,14 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 2, X.ig_pitch);
       if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 2, X.hg_pitch);
       if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
-      ce = launch_xs_grid(X, G, Ed, U, IG, HG, ubin, mconc, p->init_seed, static_cast<double *>(scratch), st);
+      put(GF_ARR_RECIP_WIDTH, Rd, npts * 8, X.n_gp);
+      ce = launch_xs_grid(X, G, Ed, Rd, zero_width, U, IG, HG, ubin, mconc, p->init_seed,
+                          static_cast<double *>(scratch), st);
+      // the exact reciprocal division is used only if no interval has zero (or underflowing) width
+      int zw = 1;
+      if (ce == cudaSuccess) ce = cudaMemcpyAsync(&zw, zero_width, sizeof(int), cudaMemcpyDeviceToHost, st);
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+      X.fastdiv = (zw == 0) ? 1 : 0;
     } else if (ce == cudaSuccess) {
       RsDev &R = g->rs;
       const int n = p->n_isotopes;
@@ -512,6 +525,22 @@ gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint
   } catch (...) {
     return fail(GF_E_NOMEM, "host allocation failed");
   }
+}
+
+gf_status gf_xs_selftest_div(const double *d_a, const double *d_b, double *d_out, double *d_ref, uint64_t n,
+                             gf_stream_t stream) {
+  if (!d_a || !d_b || !d_out || !d_ref) return fail(GF_E_INVAL, "NULL pointer");
+  if (n >= (1ull << 31)) return fail(GF_E_INVAL, "n too large");
+  if (n == 0) return GF_OK;
+  cudaError_t ce = launch_div_selftest(d_a, d_b, d_out, d_ref, (int)n, reinterpret_cast<cudaStream_t>(stream));
+  if (ce != cudaSuccess) return fail(GF_E_CUDA, "selftest launch: %s", cudaGetErrorString(ce));
+  return GF_OK;
+}
+
+gf_status gf_xs_grid_info(const gf_xs_grid *g, int32_t *fastdiv) {
+  if (!g) return fail(GF_E_INVAL, "grid is NULL");
+  if (fastdiv) *fastdiv = g->p.bench == GF_XSBENCH ? g->xs.fastdiv : 0;
+  return GF_OK;
 }
 
 gf_status gf_xs_verify(uint64_t raw_sum, uint64_t expected, uint64_t *hash) {

@@ -37,8 +37,9 @@ cudaError_t launch_tables(const double *, double *thr, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------ K0a+b
-__global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, double *__restrict__ Ed, int n_gp,
-                                                     int npow, uint64_t seed) {
+__global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, double *__restrict__ Ed,
+                                                     double *__restrict__ Rd, int *__restrict__ zero_width,
+                                                     int n_gp, int npow, uint64_t seed) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long *key = reinterpret_cast<unsigned long long *>(smem);
   uint32_t *gen = reinterpret_cast<uint32_t *>(key + npow);
@@ -91,6 +92,14 @@ __global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, dou
     rec[1] = make_double2(v[2], v[3]);
     rec[2] = make_double2(v[4], v[5]);
     Ed[(size_t)nuc * n_gp + k] = v[0];
+    // per-interval reciprocal width for the exact reciprocal division (gf_internal.cuh div_rn)
+    double r = 0.0;
+    if (k + 1 < n_gp) {
+      const double w = __dsub_rn(__longlong_as_double((long long)key[k + 1]), v[0]);
+      if (!(w >= 0x1p-960)) atomicOr(zero_width, 1);  // zero / near-underflow width: exact path off
+      r = __drcp_rn(w);
+    }
+    Rd[(size_t)nuc * n_gp + k] = r;
   }
 }
 
@@ -205,8 +214,9 @@ __global__ void concs_fill(double *__restrict__ conc, int total, uint64_t seed, 
 
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, uint16_t *IG, uint16_t *HG,
-                           uint32_t *ubin, double *mconc, uint64_t seed, double *scratch, cudaStream_t st) {
+cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, int *zero_width, double *U,
+                           uint16_t *IG, uint16_t *HG, uint32_t *ubin, double *mconc, uint64_t seed, double *scratch,
+                           cudaStream_t st) {
   cudaError_t e;
   const long long npts = (long long)X.n_iso * X.n_gp;
   int npow = 2;
@@ -215,7 +225,8 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *U, uin
   if ((e = cudaFuncSetAttribute(xs_sort_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
     return e;
   int threads = npow >= 1024 ? 1024 : (npow < 64 ? 64 : npow);
-  xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, X.n_gp, npow, seed);
+  if ((e = cudaMemsetAsync(zero_width, 0, sizeof(int), st)) != cudaSuccess) return e;
+  xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, Rd, zero_width, X.n_gp, npow, seed);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
   concs_fill<<<nblk(X.total, 256), 256, 0, st>>>(mconc, X.total, seed, 6ull * (uint64_t)npts);

@@ -11,10 +11,11 @@
 //                       nuclide bisection of the SoA energy column.
 //   A4  micro xs        per nuclide of the material, in table order: interval k (u16 index grid),
 //                       the 96-B record pair as 6 x 16-B vector loads, f and the 5 interpolations.
-//                       Software-pipelined: the record pair of nuclide j+1 and the interval of j+2
-//                       are in flight while j is computed; in the sorted kernel one thread per CTA
-//                       also issues cp.async.bulk L2 prefetches of the CTA's index-grid segments
-//                       kPrefetch nuclides ahead.
+//                       f's IEEE quotient comes from the per-interval reciprocal (div_rn, exact;
+//                       5 FP64 instructions instead of ~13).  Software-pipelined with two pair
+//                       buffers: the pair of nuclide j+1 and the interval of j+2 are in flight while
+//                       j is accumulated; the sorted unionized kernel also prefetches the index-grid
+//                       line kPrefetch nuclides ahead into L2.
 //   A5  macro xs        macro_c += micro_c * conc_c, RN multiply then RN add, j ascending.
 //   A6  hash            v = 1 + argmax (first strict max above -1.0); warp redux -> SMEM -> one u64
 //                       atomic per CTA.
@@ -26,7 +27,7 @@ namespace gf {
 
 constexpr int kRun = 8;          // consecutive lookups per thread in the sampling kernels
 constexpr int kLookupTpb = 128;  // lookup CTA size
-constexpr int kPrefetch = 16;    // nuclides of IG-segment L2 prefetch lookahead
+constexpr int kPrefetch = 8;     // nuclides of index-grid L2 prefetch lookahead
 
 // ------------------------------------------------------------------------------------------ A1/A2
 __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
@@ -185,18 +186,46 @@ __device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
 }
 
 // ------------------------------------------------------------------------------------------ A4/A5
-// Interval index k of nuclide `nuc` (clamped so that k + 1 is a gridpoint).
+// SMEM tables, XSBench flavour: per CSR entry j the nuclide's record base (nuc * n_gp) and its row
+// base in the index / hash grid (nuc * pitch), so the inner loop does 32-bit index math only.
+struct XsTables {
+  const int32_t *off;
+  const double *conc;
+  const uint2 *ent;  // {nuc * n_gp, nuc * pitch}
+  const double *thr;
+};
+
+__device__ __forceinline__ XsTables stage_xs_tables(const XsDev &X, unsigned char *smem) {
+  int32_t *s_off = reinterpret_cast<int32_t *>(smem);          // 16 ints
+  double *s_thr = reinterpret_cast<double *>(smem + 64);       // 12 doubles -> 160
+  double *s_conc = reinterpret_cast<double *>(smem + 160);     // total doubles
+  uint2 *s_ent = reinterpret_cast<uint2 *>(smem + 160 + 8 * (size_t)X.total);
+  const uint32_t pitch = (uint32_t)(X.grid_type == GF_GRID_UNIONIZED ? X.ig_pitch : X.hg_pitch);
+  for (int t = threadIdx.x; t < X.total; t += blockDim.x) {
+    const uint32_t nuc = (uint32_t)X.mnuc[t];
+    s_conc[t] = X.mconc[t];
+    s_ent[t] = make_uint2(nuc * (uint32_t)X.n_gp, nuc * pitch);
+  }
+  if (threadIdx.x < kMats + 1) s_off[threadIdx.x] = X.moff[threadIdx.x];
+  if (threadIdx.x < kMats) s_thr[threadIdx.x] = X.thr[threadIdx.x];
+  __syncthreads();
+  return XsTables{s_off, s_conc, s_ent, s_thr};
+}
+
+inline size_t xs_table_smem(int total) { return 160 + 16 * (size_t)total; }
+
+// Interval index k (clamped so that k + 1 is a gridpoint) of the nuclide of entry e.
 template <int GT>
-__device__ __forceinline__ int interval(const XsDev &X, int nuc, double E, long long idx) {
+__device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, long long idx) {
   const int n_gp = X.n_gp;
   int k;
   if (GT == GF_GRID_NUCLIDE) {
-    k = bisect<int>(X.Ed + (size_t)nuc * n_gp, E, 0, n_gp - 1);
+    k = bisect<int>(X.Ed + e.x, E, 0, n_gp - 1);
   } else if (GT == GF_GRID_UNIONIZED) {
-    k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + idx);
+    k = __ldg(X.IG + e.y + (uint32_t)idx);
   } else {
-    const double *Ed = X.Ed + (size_t)nuc * n_gp;
-    const uint16_t *hg = X.HG + (size_t)nuc * X.hg_pitch + idx;
+    const double *Ed = X.Ed + e.x;
+    const uint16_t *hg = X.HG + e.y + (uint32_t)idx;
     const int lo_ = __ldg(hg);
     const int hi_ = (idx == X.bins - 1) ? n_gp - 1 : (int)__ldg(hg + 1) + 1;
     if (E <= __ldg(Ed + lo_))
@@ -206,28 +235,32 @@ __device__ __forceinline__ int interval(const XsDev &X, int nuc, double E, long 
     else
       k = bisect<int>(Ed, E, lo_, hi_);
   }
-  return k == n_gp - 1 ? k - 1 : k;
+  return (uint32_t)(k == n_gp - 1 ? k - 1 : k);
 }
 
-struct Pair {  // records k (lo) and k+1 (hi): E, total, elastic, absorption, fission, nu-fission
+struct Pair {  // records k (lo) and k+1 (hi): E, total, elastic, absorption, fission, nu-fission; y
   double2 l0, l1, l2, h0, h1, h2;
+  double y;    // RN(1 / (hi.E - lo.E)) (fast division path only)
 };
 
-__device__ __forceinline__ Pair load_pair(const XsDev &X, int nuc, int k) {
-  const double2 *p = reinterpret_cast<const double2 *>(X.G + ((size_t)nuc * X.n_gp + k) * 6);
-  Pair P;
+template <bool FAST>
+__device__ __forceinline__ void load_pair(const XsDev &X, uint32_t rec, Pair &P) {
+  const double2 *p = reinterpret_cast<const double2 *>(X.G) + (size_t)rec * 3;
   P.l0 = __ldg(p + 0);
   P.l1 = __ldg(p + 1);
   P.l2 = __ldg(p + 2);
   P.h0 = __ldg(p + 3);
   P.h1 = __ldg(p + 4);
   P.h2 = __ldg(p + 5);
-  return P;
+  if (FAST) P.y = __ldg(X.Rd + rec);
 }
 
-// f = (hi.E - E) / (hi.E - lo.E); x_c = hi_c - f (hi_c - lo_c); m_c += x_c * conc (all RN, no FMA).
+// f = (hi.E - E) / (hi.E - lo.E); x_c = hi_c - f (hi_c - lo_c); m_c += x_c * conc, every operation
+// rounded to nearest and none contracted; the quotient is IEEE RN either way (div_rn is exact).
+template <bool FAST>
 __device__ __forceinline__ void accumulate(const Pair &P, double E, double conc, double m[5]) {
-  const double f = __ddiv_rn(__dsub_rn(P.h0.x, E), __dsub_rn(P.h0.x, P.l0.x));
+  const double a = __dsub_rn(P.h0.x, E), b = __dsub_rn(P.h0.x, P.l0.x);
+  const double f = FAST ? div_rn(a, b, P.y) : __ddiv_rn(a, b);
   const double lo[5] = {P.l0.y, P.l1.x, P.l1.y, P.l2.x, P.l2.y};
   const double hi[5] = {P.h0.y, P.h1.x, P.h1.y, P.h2.x, P.h2.y};
 #pragma unroll
@@ -237,38 +270,43 @@ __device__ __forceinline__ void accumulate(const Pair &P, double E, double conc,
   }
 }
 
-// CTA-level L2 prefetch of the index-grid row segment [lo, hi) (u16 entries, 16-B aligned) of the
-// nuclide at table entry j, issued by one thread (cp.async.bulk.prefetch: no registers, no SMEM).
-struct Prefetch {
-  bool on;
-  long long lo, hi;
-};
-
-__device__ __forceinline__ void prefetch_ig(const XsDev &X, const Tables &T, const Prefetch &pf, int j) {
-  const uint16_t *a = X.IG + (size_t)T.nuc[j] * X.ig_pitch + pf.lo;
-  const uint32_t bytes = (uint32_t)((pf.hi - pf.lo) * 2);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+// Nuclides j0..j1-1 in table order, software-pipelined with two record-pair buffers (A, B): the
+// pair of j+1 and the interval of j+2 are loaded while j is accumulated.  With PF, each thread also
+// prefetches into L2 the index-grid line of nuclide j + kPrefetch.
+template <int GT, bool FAST, bool PF>
+__device__ __forceinline__ void nuclide_loop(const XsDev &X, const XsTables &T, double E, long long idx, int j0,
+                                             int j1, double m[5]) {
+  Pair A, B;
+  uint32_t kA = interval<GT>(X, T.ent[j0], E, idx);
+  load_pair<FAST>(X, T.ent[j0].x + kA, A);
+  uint32_t kB = (j0 + 1 < j1) ? interval<GT>(X, T.ent[j0 + 1], E, idx) : 0u;
+  for (int j = j0; j < j1; j += 2) {
+    if (PF && j + kPrefetch < j1)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(X.IG + T.ent[j + kPrefetch].y + (uint32_t)idx));
+    if (j + 1 < j1) load_pair<FAST>(X, T.ent[j + 1].x + kB, B);
+    if (j + 2 < j1) kA = interval<GT>(X, T.ent[j + 2], E, idx);
+    accumulate<FAST>(A, E, T.conc[j], m);
+    if (j + 1 >= j1) break;
+    if (PF && j + 1 + kPrefetch < j1)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(X.IG + T.ent[j + 1 + kPrefetch].y + (uint32_t)idx));
+    if (j + 2 < j1) load_pair<FAST>(X, T.ent[j + 2].x + kA, A);
+    if (j + 3 < j1) kB = interval<GT>(X, T.ent[j + 3], E, idx);
+    accumulate<FAST>(B, E, T.conc[j + 1], m);
+  }
 }
 
-template <int GT>
-__device__ __forceinline__ void macro_xs(const XsDev &X, const Tables &T, double E, long long idx, int mat,
-                                         double m[5], const Prefetch &pf) {
+template <int GT, bool PF>
+__device__ __forceinline__ void macro_xs(const XsDev &X, const XsTables &T, double E, long long idx, int mat,
+                                         double m[5]) {
 #pragma unroll
   for (int c = 0; c < 5; c++) m[c] = 0.0;
   const int j0 = T.off[mat], j1 = T.off[mat + 1];
   if (j0 >= j1) return;
-  // pipeline: pair(j+1) and interval(j+2) are in flight while j is accumulated
-  Pair nxt = load_pair(X, T.nuc[j0], interval<GT>(X, T.nuc[j0], E, idx));
-  int k2 = (j0 + 1 < j1) ? interval<GT>(X, T.nuc[j0 + 1], E, idx) : 0;
-  for (int j = j0; j < j1; j++) {
-    const Pair cur = nxt;
-    const double conc = T.conc[j];
-    if (GT == GF_GRID_UNIONIZED && pf.on && threadIdx.x == 0 && j + kPrefetch < j1)
-      prefetch_ig(X, T, pf, j + kPrefetch);
-    if (j + 1 < j1) nxt = load_pair(X, T.nuc[j + 1], k2);
-    if (j + 2 < j1) k2 = interval<GT>(X, T.nuc[j + 2], E, idx);
-    accumulate(cur, E, conc, m);
-  }
+  // the reciprocal division needs |hi.E - E| <= 4 (all sampled energies are in [0, 1])
+  if (X.fastdiv && fabs(E) <= 2.0)
+    nuclide_loop<GT, true, PF>(X, T, E, idx, j0, j1, m);
+  else
+    nuclide_loop<GT, false, PF>(X, T, E, idx, j0, j1, m);
 }
 
 __device__ __forceinline__ uint32_t argmax5_plus1(const double m[5]) {
@@ -292,7 +330,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
                                                                double *__restrict__ macro_out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Tables T = stage_tables(X.total, X.moff, X.mnuc, X.mconc, X.thr, smem);
+  const XsTables T = stage_xs_tables(X, smem);
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t v = 0;
   if (t < n) {
@@ -308,7 +346,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
       mat = pick_material(lcg_draw(s), T.thr);
     }
     double m[5];
-    macro_xs<GT>(X, T, E, energy_index<GT>(X, E), mat, m, Prefetch{false, 0, 0});
+    macro_xs<GT, false>(X, T, E, energy_index<GT>(X, E), mat, m);
     v = argmax5_plus1(m);
     if (macro_out) {
 #pragma unroll
@@ -327,43 +365,17 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
                                                                double *__restrict__ macro_out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_mat[2];
-  __shared__ unsigned long long s_ulo, s_uhi;
-  const Tables T = stage_tables(X.total, X.moff, X.mnuc, X.mconc, X.thr, smem);
-  const uint32_t p0 = blockIdx.x * blockDim.x;
-  const uint32_t p = p0 + threadIdx.x;
-  const uint32_t pc = min(p, min(n, p0 + blockDim.x) - 1);  // clamped: tail threads mirror the last lookup
-  int mat = 0;
-#pragma unroll
-  for (int m = 1; m < kMats; m++)
-    if (pc >= __ldg(mstart + m)) mat = m;
-  const double E = Es[pc];
-  const long long u = energy_index<GT>(X, E);
-  Prefetch pf{false, 0, 0};
-  if (GT == GF_GRID_UNIONIZED) {
-    // CTA-uniform material: prefetch the CTA's index-grid segments into L2 ahead of use.
-    if (threadIdx.x == 0) {
-      s_mat[0] = mat;
-      s_ulo = ~0ull;
-      s_uhi = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_mat[1] = mat;
-    atomicMin(&s_ulo, (unsigned long long)u);
-    atomicMax(&s_uhi, (unsigned long long)u);
-    __syncthreads();
-    if (s_mat[0] == s_mat[1]) {
-      pf.on = true;
-      pf.lo = (long long)(s_ulo & ~7ull);
-      pf.hi = (long long)((s_uhi + 8) & ~7ull);
-      const int j0 = T.off[mat], j1 = T.off[mat + 1];
-      if ((int)threadIdx.x < kPrefetch && j0 + (int)threadIdx.x < j1) prefetch_ig(X, T, pf, j0 + threadIdx.x);
-    }
-  }
+  const XsTables T = stage_xs_tables(X, smem);
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t v = 0;
   if (p < n) {
+    int mat = 0;
+#pragma unroll
+    for (int mm = 1; mm < kMats; mm++)
+      if (p >= __ldg(mstart + mm)) mat = mm;
+    const double E = Es[p];
     double m[5];
-    macro_xs<GT>(X, T, E, u, mat, m, pf);
+    macro_xs<GT, GT == GF_GRID_UNIONIZED>(X, T, E, energy_index<GT>(X, E), mat, m);
     v = argmax5_plus1(m);
     if (macro_out) {
       const size_t o = (size_t)idx[p] * 5;
@@ -378,7 +390,7 @@ template <int GT>
 static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                              const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
                              unsigned long long *vsum, cudaStream_t st, cudaEvent_t ev_mid) {
-  const size_t smem = table_smem(X.total);
+  const size_t smem = xs_table_smem(X.total);
   cudaError_t e;
   if (sort) {
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, macro_out != nullptr, st)) != cudaSuccess)
@@ -404,6 +416,20 @@ cudaError_t launch_xs_lookup(const XsDev &X, uint64_t first, uint32_t n, uint64_
     default:
       return launch_gt<GF_GRID_HASH>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
   }
+}
+
+// Self-test hook for the exact reciprocal division (tests): out[i] = div_rn(a[i], b[i], RN(1/b[i]))
+// and ref[i] = __ddiv_rn(a[i], b[i]).
+__global__ void div_selftest(const double *a, const double *b, double *out, double *ref, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = div_rn(a[i], b[i], __drcp_rn(b[i]));
+  ref[i] = __ddiv_rn(a[i], b[i]);
+}
+
+cudaError_t launch_div_selftest(const double *a, const double *b, double *out, double *ref, int n, cudaStream_t st) {
+  div_selftest<<<nblk(n, 256), 256, 0, st>>>(a, b, out, ref, n);
+  return cudaGetLastError();
 }
 
 }  // namespace gf

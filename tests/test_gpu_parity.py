@@ -66,6 +66,11 @@ def check_arrays(o, g, full_ig=True):
     n_iso, n_gp = o.n_iso, o.n_gp
     G = g.array("nuclide_grid")[0].cpu().numpy().reshape(n_iso, n_gp, 6)
     assert np.array_equal(G, o.nuclide_grid())
+    R = g.array("recip_width")[0].cpu().numpy().reshape(n_iso, n_gp)
+    w = np.diff(G[:, :, 0], axis=1)
+    with np.errstate(divide="ignore"):
+        assert np.array_equal(R[:, :-1], 1.0 / w)  # correctly rounded reciprocal widths
+    assert g.fastdiv == bool(np.all(w >= 2.0 ** -960))
     Ed = g.array("energy")[0].cpu().numpy().reshape(n_iso, n_gp)
     assert np.array_equal(Ed, o.nuclide_grid()[:, :, 0])
     nn, mats, concs = o.tables()
@@ -141,6 +146,41 @@ def test_n_zero_and_flags(gf, torch):
         gf._check(gf.lib().gf_xs_lookup_batch(g.h, 0, 1 << 32, 1070, 0, None, C.c_void_p(v.data_ptr()),
                                               C.c_void_p(sc.data_ptr()), sc.numel(), None))
     assert e.value.status == 1
+
+
+def test_div_rn_matches_ieee(gf, torch):
+    """The lookup kernels' reciprocal division (q0 = a y, two FMA corrections, y = RN(1/b)) equals
+    IEEE a / b bit for bit: random operands, binade-edge adversarial operands, and the real (a, b)
+    pairs of a large grid's intervals."""
+    import ctypes as C
+    rng = np.random.default_rng(12)
+    n = 2_000_000
+    a1 = rng.uniform(-4, 4, n)
+    b1 = np.ldexp(1 + rng.random(n), rng.integers(-900, 3, n))
+    # b just above a power of two, a/b just below the next one (the worst case of q0 = RN(a y))
+    e = rng.integers(-60, 1, n)
+    b2 = np.ldexp(1 + rng.random(n) * 2.0 ** -20, e)
+    x = np.ldexp(2 - rng.random(n) * 2.0 ** -20, rng.integers(-6, 2, n))
+    a2 = np.clip(x * b2, -4, 4)
+    o = O.XSOracle(355, 11303, O.NUCLIDE)
+    G = o.nuclide_grid()[:, :, 0]
+    nuc = rng.integers(0, 355, n)
+    k = rng.integers(0, 11302, n)
+    lo, hi = G[nuc, k], G[nuc, k + 1]
+    E = lo + (hi - lo) * rng.uniform(-0.5, 1.5, n)
+    b3 = hi - lo
+    a3 = hi - E
+    a = np.concatenate([a1, a2, a3, [0.0, -0.0, 4.0, -4.0]])
+    b = np.concatenate([b1, b2, b3, [1.0, 3.0, 2.0 ** -900, 1.0 - 2.0 ** -53]])
+    keep = b >= 2.0 ** -960
+    a, b = a[keep], b[keep]
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out, ref = torch.empty_like(da), torch.empty_like(da)
+    gf._check(gf.lib().gf_xs_selftest_div(C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()),
+                                          C.c_void_p(out.data_ptr()), C.c_void_p(ref.data_ptr()), len(a), None))
+    out, ref = out.cpu().numpy(), ref.cpu().numpy()
+    assert np.array_equal(out.view(np.int64), ref.view(np.int64))
+    assert np.array_equal(ref, a / b)  # numpy's division is IEEE RN too
 
 
 # ------------------------------------------------------------------------------------------ paper shapes

@@ -147,7 +147,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     const size_t npts = (size_t)p->n_isotopes * (size_t)p->n_gridpoints;
     L.G = take(npts * 48);
     L.Ed = take(npts * 8);
-    L.Rd = take(npts * 8);
+    L.Rd = take(npts * 8 + 16);  // +16: the staged kernel's bulk copies round ranges up to 16 B
     L.flags = take(16);
     if (p->grid_type == GF_GRID_UNIONIZED) {
       L.ig_pitch = (long long)((npts + 63) & ~size_t(63));

@@ -212,7 +212,7 @@ __device__ __forceinline__ XsTables stage_xs_tables(const XsDev &X, unsigned cha
   return XsTables{s_off, s_conc, s_ent, s_thr};
 }
 
-inline size_t xs_table_smem(int total) { return 160 + 16 * (size_t)total; }
+__host__ __device__ inline size_t xs_table_smem(int total) { return 160 + 16 * (size_t)total; }
 
 // Interval index k (clamped so that k + 1 is a gridpoint) of the nuclide of entry e.
 template <int GT>
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
                                                                const uint8_t *__restrict__ src_mat,
                                                                double *__restrict__ macro_out,
                                                                unsigned long long *__restrict__ vsum) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t v = 0;
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
                                                                const uint32_t *__restrict__ mstart,
                                                                double *__restrict__ macro_out,
                                                                unsigned long long *__restrict__ vsum) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t v = 0;
@@ -386,6 +386,283 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
   hash_epilogue(v, vsum);
 }
 
+// ------------------------------------------------------------------------------------------ staged
+// xs_lookup_staged: the sorted unionized lookup with the memory side moved to the TMA engine.
+//
+// Persistent CTAs of 4 consumer warps + 1 producer warp walk tiles of kTile consecutive sorted
+// lookups.  A tile whose lookups share one material and whose unionized indices span <= kIgCap
+// entries is "staged": for each nuclide j of the material, the producer (one lane) issues
+//   (1) cp.async.bulk of the CTA's index-grid row segment IG[nuc][u_lo..u_hi] into SMEM stage s,
+//   (2) once it has landed, cp.async.bulk of the record range [k_lo, k_hi + 1] of the nuclide grid
+//       (k_lo = IG[u_lo], k_hi = IG[u_hi]: the index grid is monotone in u) and of the matching
+//       reciprocal widths,
+// through a ring of kStages SMEM stages guarded by mbarriers (full_ig / full: transaction-count
+// completion of the bulk copies; empty: one arrival per consumer warp).  Consumers read their
+// interval index and record pair from SMEM (records past kRecCap fall back to global loads), so
+// every global access on the hot path is an asynchronous bulk copy.  Other tiles (mixed material,
+// sparse materials with wide index ranges) run the per-thread pipelined loop (nuclide_loop).
+// Results are identical to xs_lookup_sorted: same interval index, same arithmetic, same order.
+constexpr int kTile = 128;           // lookups per tile = consumer threads
+constexpr int kStagedThreads = kTile + 32;
+constexpr int kStages = 16;
+constexpr int kIgCap = 1024;         // index-grid entries per stage (2 KB)
+constexpr int kRecCap = 8;           // records per stage (k_hi - k_lo + 2 <= kRecCap covers >99.9%)
+constexpr int kRdCap = kRecCap + 2;  // reciprocal widths per stage (range rounded to 16 B)
+// stage layout: ig[kIgCap] u16 | rec[kRecCap] 48-B records | rd[kRdCap] f64 | StageMeta (16 B)
+constexpr int kStageBytes = (2 * kIgCap + 48 * kRecCap + 8 * kRdCap + 16 + 127) & ~127;
+static_assert((2 * kIgCap) % 16 == 0 && (48 * kRecCap) % 16 == 0 && (8 * kRdCap) % 16 == 0,
+              "bulk-copy destinations must stay 16-B aligned");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+struct StageMeta {
+  int k_lo;    // record index (within the nuclide) of rec[0]
+  int n_rec;   // records staged
+  uint32_t rd_lo;  // absolute index (into Rd) of rd[0]
+  int pad;
+};
+
+inline size_t staged_smem(int total) {
+  size_t t = (xs_table_smem(total) + 15) & ~size_t(15);
+  t += 3 * kStages * 8;
+  t = (t + 127) & ~size_t(127);
+  return t + (size_t)kStages * kStageBytes;
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(kStagedThreads, 3)
+    xs_lookup_staged(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ idx,
+                     const uint32_t *__restrict__ mstart, double *__restrict__ macro_out,
+                     unsigned long long *__restrict__ vsum) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const XsTables T = stage_xs_tables(X, smem);
+  size_t off = (xs_table_smem(X.total) + 15) & ~size_t(15);
+  uint64_t *full_ig = reinterpret_cast<uint64_t *>(smem + off);
+  uint64_t *full = full_ig + kStages;
+  uint64_t *empty = full + kStages;
+  off = (off + 3 * kStages * 8 + 127) & ~size_t(127);
+  unsigned char *stages = smem + off;
+  __shared__ uint32_t s_ulo[2], s_uhi[2];
+  __shared__ int s_mlo[2], s_mhi[2];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full_ig[s], 1);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTile / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 2) {
+    s_ulo[tid] = 0xFFFFFFFFu;
+    s_uhi[tid] = 0;
+    s_mlo[tid] = -1;
+    s_mhi[tid] = -1;
+  }
+  __syncthreads();
+
+  const uint32_t ntiles = (n + kTile - 1) / kTile;
+  uint32_t it = 0;   // staged items consumed / produced so far (ring position)
+  uint32_t vacc = 0;
+  int tp = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tp ^= 1) {
+    const uint32_t p0 = tile * kTile;
+    const uint32_t plast = min(n, p0 + kTile) - 1;
+    uint32_t p = p0 + tid, pc = min(p, plast);
+    int mat = 0;
+    double E = 0.0;
+    uint32_t u = 0;
+    if (warp < kTile / 32) {
+#pragma unroll
+      for (int mm = 1; mm < kMats; mm++)
+        if (pc >= __ldg(mstart + mm)) mat = mm;
+      E = Es[pc];
+      u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
+      atomicMin(&s_ulo[tp], u);
+      atomicMax(&s_uhi[tp], u);
+      if (pc == p0) s_mlo[tp] = mat;
+      if (pc == plast && p == plast) s_mhi[tp] = mat;
+    }
+    named_sync(1, kStagedThreads);
+    const uint32_t ulo = s_ulo[tp], uhi = s_uhi[tp];
+    const int mlo = s_mlo[tp], mhi = s_mhi[tp];
+    if (tid == 0) {
+      s_ulo[tp ^ 1] = 0xFFFFFFFFu;
+      s_uhi[tp ^ 1] = 0;
+    }
+    const uint32_t ubase = ulo & ~7u;
+    const uint32_t uend = (uhi + 8) & ~7u;  // exclusive, 16-B multiple
+    const int j0 = T.off[mlo], j1 = T.off[mlo + 1];
+    const bool staged = (mlo == mhi) && (uend - ubase <= (uint32_t)kIgCap) && (j1 > j0);
+    const int cnt = staged ? j1 - j0 : 0;
+
+    if (warp == kTile / 32) {
+      // ---------------------------------------------------------------- producer (one lane)
+      if (lane == 0 && staged) {
+        const uint32_t ig_bytes = (uend - ubase) * 2;
+        int issued = 0, done = 0;
+        while (done < cnt) {
+          while (issued < cnt && issued - done < kStages) {
+            const uint32_t g = it + issued, s = g % kStages, ph = (g / kStages) & 1u;
+            if (!mbar_test(&empty[s], ph ^ 1u)) break;
+            unsigned char *st = stages + (size_t)s * kStageBytes;
+            mbar_arrive_tx(&full_ig[s], ig_bytes);
+            bulk_g2s(st, X.IG + T.ent[j0 + issued].y + ubase, ig_bytes, &full_ig[s]);
+            issued++;
+          }
+          if (issued == done) continue;  // every stage busy: poll again
+          const uint32_t g = it + done, s = g % kStages, ph = (g / kStages) & 1u;
+          if (!mbar_test(&full_ig[s], ph)) continue;
+          unsigned char *st = stages + (size_t)s * kStageBytes;
+          const uint16_t *ig = reinterpret_cast<const uint16_t *>(st);
+          const int klo = ig[ulo - ubase], khi = ig[uhi - ubase];
+          const int nrec = min(khi + 2 - klo, kRecCap);
+          const uint32_t rec0 = T.ent[j0 + done].x + (uint32_t)klo;
+          const uint32_t rdlo = rec0 & ~1u;
+          const uint32_t rdn = (rec0 + (uint32_t)nrec - rdlo + 1u) & ~1u;
+          StageMeta *meta = reinterpret_cast<StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
+          meta->k_lo = klo;
+          meta->n_rec = nrec;
+          meta->rd_lo = rdlo;
+          mbar_arrive_tx(&full[s], (uint32_t)nrec * 48u + (FAST ? rdn * 8u : 0u));
+          bulk_g2s(st + 2 * kIgCap, X.G + (size_t)rec0 * 6, (uint32_t)nrec * 48u, &full[s]);
+          if (FAST) bulk_g2s(st + 2 * kIgCap + 48 * kRecCap, X.Rd + rdlo, rdn * 8u, &full[s]);
+          done++;
+        }
+      }
+      __syncwarp();
+    } else {
+      // ---------------------------------------------------------------- consumers
+      double m[5];
+#pragma unroll
+      for (int c = 0; c < 5; c++) m[c] = 0.0;
+      const bool fast = FAST && fabs(E) <= 2.0;
+      if (staged) {
+        const uint32_t urel = u - ubase;
+        for (int q = 0; q < cnt; q++) {
+          const uint32_t g = it + q, s = g % kStages, ph = (g / kStages) & 1u;
+          const unsigned char *st = stages + (size_t)s * kStageBytes;
+          mbar_wait(&full_ig[s], ph);
+          mbar_wait(&full[s], ph);
+          const StageMeta meta = *reinterpret_cast<const StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
+          const uint32_t k = reinterpret_cast<const uint16_t *>(st)[urel];
+          const int rel = (int)k - meta.k_lo;
+          const uint2 e = T.ent[j0 + q];
+          Pair P;
+          if (rel + 1 < meta.n_rec) {
+            const double2 *r = reinterpret_cast<const double2 *>(st + 2 * kIgCap) + rel * 3;
+            P.l0 = r[0]; P.l1 = r[1]; P.l2 = r[2]; P.h0 = r[3]; P.h1 = r[4]; P.h2 = r[5];
+            if (FAST) P.y = reinterpret_cast<const double *>(st + 2 * kIgCap + 48 * kRecCap)[e.x + k - meta.rd_lo];
+          } else {
+            load_pair<FAST>(X, e.x + k, P);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          if (fast)
+            accumulate<true>(P, E, T.conc[j0 + q], m);
+          else
+            accumulate<false>(P, E, T.conc[j0 + q], m);
+        }
+      } else if (mat >= 0) {
+        const int a0 = T.off[mat], a1 = T.off[mat + 1];
+        if (a1 > a0) {
+          if (fast)
+            nuclide_loop<GF_GRID_UNIONIZED, true, false>(X, T, E, u, a0, a1, m);
+          else
+            nuclide_loop<GF_GRID_UNIONIZED, false, false>(X, T, E, u, a0, a1, m);
+        }
+      }
+      if (p < n) {
+        vacc += argmax5_plus1(m);
+        if (macro_out) {
+          const size_t o = (size_t)idx[p] * 5;
+#pragma unroll
+          for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
+        }
+      }
+    }
+    it += (uint32_t)cnt;
+    if (tid == 0) {
+      s_mlo[tp ^ 1] = -1;
+      s_mhi[tp ^ 1] = -1;
+    }
+    named_sync(1, kStagedThreads);  // the next tile reuses the other slot; keep the warps in step
+  }
+  hash_epilogue(vacc, vsum);
+}
+
+template <bool FAST>
+static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &S, double *macro_out,
+                                 unsigned long long *vsum, cudaStream_t st) {
+  const size_t smem = staged_smem(X.total);
+  static int blocks_per_sm[2] = {0, 0};
+  static size_t smem_cfg[2] = {0, 0};
+  cudaError_t e;
+  if (smem_cfg[FAST] != smem) {
+    if ((e = cudaFuncSetAttribute(xs_lookup_staged<FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[FAST], xs_lookup_staged<FAST>,
+                                                           kStagedThreads, smem)) != cudaSuccess)
+      return e;
+    smem_cfg[FAST] = smem;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t ntiles = (n + kTile - 1) / kTile;
+  const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm[FAST], 1)));
+  xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
+  return cudaGetLastError();
+}
+
+// GF_XS_STAGED=0 in the environment selects the per-thread kernel for the sorted unionized path
+// (A/B measurements); the default is the staged kernel.
+static bool use_staged() {
+  static int v = -1;
+  if (v < 0) {
+    const char *s = getenv("GF_XS_STAGED");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int GT>
 static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                              const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
@@ -396,6 +673,9 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, macro_out != nullptr, st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
+    if (GT == GF_GRID_UNIONIZED && use_staged())
+      return X.fastdiv ? launch_staged<true>(X, n, S, macro_out, vsum, st)
+                       : launch_staged<false>(X, n, S, macro_out, vsum, st);
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;

@@ -92,7 +92,7 @@ def test_grid_bytes_closed_form():
         assert st == 0
         npts = n_iso * 11303
         total = (34 if n_iso == 68 else 321) + 5 + 4 + 4 + 27 + 5 * 21 + 2 * 9
-        want = al(npts * 48) + al(npts * 8)
+        want = al(npts * 48) + al(npts * 8) + al(npts * 8) + al(16)  # G, Ed, reciprocal widths, flags
         if gt == gf.UNIONIZED:
             pitch = (npts + 63) // 64 * 64
             want += al(npts * 8) + al(n_iso * pitch * 2) + al(16385 * 4)
@@ -100,9 +100,9 @@ def test_grid_bytes_closed_form():
             want += al(n_iso * 10048 * 2)
         want += al(128) + al(64) + al(total * 4) + al(total * 8)
         assert gb == want, (n_iso, gt)
-    # C3: the 355 x 4,012,565 u16 index grid (2.85 GB) dominates the 3.10 GB total
+    # C3: the 355 x 4,012,565 u16 index grid (2.85 GB) dominates the 3.13 GB total
     st, gb, _ = _bytes(gf.Params.xsbench(355, 11303, gf.UNIONIZED))
-    assert 3.09e9 < gb < 3.11e9
+    assert 3.12e9 < gb < 3.14e9
 
 
 @pytest.mark.parametrize("field,value,status", [

@@ -464,6 +464,34 @@ inline size_t staged_smem(int total) {
   return t + (size_t)kStages * kStageBytes;
 }
 
+// Tile facts both sides derive identically: material of the first / last lookup and the index
+// range [energy_index(min E), energy_index(max E)] (energy_index is monotone in E).
+struct TileInfo {
+  int staged, j0, cnt;
+  uint32_t ubase, ulo, uhi;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const XsTables &T, int mlo, int mhi, uint32_t ulo, uint32_t uhi) {
+  TileInfo t;
+  t.ubase = ulo & ~7u;
+  t.ulo = ulo;
+  t.uhi = uhi;
+  const uint32_t uend = (uhi + 8) & ~7u;
+  t.j0 = T.off[mlo];
+  const int j1 = T.off[mlo + 1];
+  t.staged = (mlo == mhi) && (uend - t.ubase <= (uint32_t)kIgCap) && (j1 > t.j0);
+  t.cnt = t.staged ? j1 - t.j0 : 0;
+  return t;
+}
+
+__device__ __forceinline__ int material_of(const uint32_t *mstart, uint32_t p) {
+  int mat = 0;
+#pragma unroll
+  for (int mm = 1; mm < kMats; mm++)
+    if (p >= __ldg(mstart + mm)) mat = mm;
+  return mat;
+}
+
 template <bool FAST>
 __global__ void __launch_bounds__(kStagedThreads, 3)
     xs_lookup_staged(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ idx,
@@ -478,7 +506,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   off = (off + 3 * kStages * 8 + 127) & ~size_t(127);
   unsigned char *stages = smem + off;
   __shared__ uint32_t s_ulo[2], s_uhi[2];
-  __shared__ int s_mlo[2], s_mhi[2];
+  __shared__ TileInfo s_ring[kStages];  // producer-private: tile facts of in-flight items
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -492,137 +520,175 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   if (tid < 2) {
     s_ulo[tid] = 0xFFFFFFFFu;
     s_uhi[tid] = 0;
-    s_mlo[tid] = -1;
-    s_mhi[tid] = -1;
   }
   __syncthreads();
-
   const uint32_t ntiles = (n + kTile - 1) / kTile;
-  uint32_t it = 0;   // staged items consumed / produced so far (ring position)
+
+  if (warp == kTile / 32) {
+    // ================================================================ producer warp
+    // Walks the CTA's tiles in the consumers' order; cursor A issues index-grid segments up to
+    // kLook items ahead of cursor B, which issues record ranges once a segment has landed.  All
+    // lanes run the control flow (tile facts are a warp reduction); lane 0 issues.
+    constexpr int kLook = kStages - 2;
+    uint32_t tA = blockIdx.x;                   // tile of cursor A
+    int qA = 0, qB = 0;                         // item within the tile
+    uint32_t gA = 0, gB = 0;                    // global item counters
+    TileInfo iA{0, 0, 0, 0, 0, 0}, iB{0, 0, 0, 0, 0, 0};
+    bool haveA = false, haveB = false;
+    uint32_t ringA = 0, ringB = 0;  // tile-info ring slots (tiles entered by A / B)
+    auto info_of = [&](uint32_t tile) {
+      const uint32_t p0 = tile * kTile, plast = min(n, p0 + kTile) - 1;
+      double lo = 3.0e300, hi = -3.0e300;
+      for (uint32_t p = p0 + lane; p <= plast; p += 32) {
+        const double e = Es[p];
+        lo = fmin(lo, e);
+        hi = fmax(hi, e);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      const uint32_t ulo = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, lo);
+      const uint32_t uhi = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, hi);
+      return tile_info(T, material_of(mstart, p0), material_of(mstart, plast), ulo, uhi);
+    };
+    // Advance a cursor to its next staged item; false at the end of the CTA's tiles.  Only staged
+    // tiles enter the ring, so it holds at most kLook + 1 <= kStages tiles between B and A.
+    auto advanceA = [&]() -> bool {
+      while (true) {
+        if (haveA && qA < iA.cnt) return true;
+        if (haveA) tA += gridDim.x;
+        if (tA >= ntiles) return false;
+        iA = info_of(tA);
+        haveA = true;
+        qA = 0;
+        if (iA.cnt > 0) {
+          if (lane == 0) s_ring[ringA % kStages] = iA;
+          ringA++;
+        }
+      }
+    };
+    auto advanceB = [&]() -> bool {
+      if (haveB && qB < iB.cnt) return true;
+      if (ringB == ringA) return false;
+      __syncwarp();
+      iB = s_ring[ringB % kStages];
+      ringB++;
+      haveB = true;
+      qB = 0;
+      return true;
+    };
+    bool moreA = advanceA();
+    while (true) {
+      // cursor A: index-grid segments, at most kLook items ahead of B
+      while (moreA && gA < gB + kLook) {
+        const uint32_t s = gA % kStages, ph = (gA / kStages) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        if (lane == 0) {
+          const uint32_t bytes = (((iA.uhi + 8) & ~7u) - iA.ubase) * 2;
+          mbar_arrive_tx(&full_ig[s], bytes);
+          bulk_g2s(stages + (size_t)s * kStageBytes, X.IG + T.ent[iA.j0 + qA].y + iA.ubase, bytes, &full_ig[s]);
+        }
+        gA++;
+        qA++;
+        moreA = advanceA();
+      }
+      if (gB == gA) break;  // A exhausted and B caught up
+      if (!advanceB()) break;
+      // cursor B: record range of item gB once its index-grid segment has landed
+      const uint32_t s = gB % kStages, ph = (gB / kStages) & 1u;
+      mbar_wait(&full_ig[s], ph);
+      if (lane == 0) {
+        unsigned char *st = stages + (size_t)s * kStageBytes;
+        const uint16_t *ig = reinterpret_cast<const uint16_t *>(st);
+        const int klo = ig[iB.ulo - iB.ubase], khi = ig[iB.uhi - iB.ubase];
+        const int nrec = min(khi + 2 - klo, kRecCap);
+        const uint32_t rec0 = T.ent[iB.j0 + qB].x + (uint32_t)klo;
+        const uint32_t rdlo = rec0 & ~1u;
+        const uint32_t rdn = (rec0 + (uint32_t)nrec - rdlo + 1u) & ~1u;
+        StageMeta *meta = reinterpret_cast<StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
+        meta->k_lo = klo;
+        meta->n_rec = nrec;
+        meta->rd_lo = rdlo;
+        mbar_arrive_tx(&full[s], (uint32_t)nrec * 48u + (FAST ? rdn * 8u : 0u));
+        bulk_g2s(st + 2 * kIgCap, X.G + (size_t)rec0 * 6, (uint32_t)nrec * 48u, &full[s]);
+        if (FAST) bulk_g2s(st + 2 * kIgCap + 48 * kRecCap, X.Rd + rdlo, rdn * 8u, &full[s]);
+      }
+      __syncwarp();
+      gB++;
+      qB++;
+    }
+    hash_epilogue(0u, vsum);
+    return;
+  }
+
+  // ================================================================== consumer warps
+  uint32_t it = 0;  // staged items consumed so far (ring position)
   uint32_t vacc = 0;
   int tp = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tp ^= 1) {
     const uint32_t p0 = tile * kTile;
     const uint32_t plast = min(n, p0 + kTile) - 1;
-    uint32_t p = p0 + tid, pc = min(p, plast);
-    int mat = 0;
-    double E = 0.0;
-    uint32_t u = 0;
-    if (warp < kTile / 32) {
-#pragma unroll
-      for (int mm = 1; mm < kMats; mm++)
-        if (pc >= __ldg(mstart + mm)) mat = mm;
-      E = Es[pc];
-      u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
-      atomicMin(&s_ulo[tp], u);
-      atomicMax(&s_uhi[tp], u);
-      if (pc == p0) s_mlo[tp] = mat;
-      if (pc == plast && p == plast) s_mhi[tp] = mat;
-    }
-    named_sync(1, kStagedThreads);
-    const uint32_t ulo = s_ulo[tp], uhi = s_uhi[tp];
-    const int mlo = s_mlo[tp], mhi = s_mhi[tp];
-    if (tid == 0) {
+    const uint32_t p = p0 + tid, pc = min(p, plast);
+    const int mat = material_of(mstart, pc);
+    const double E = Es[pc];
+    const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
+    atomicMin(&s_ulo[tp], u);
+    atomicMax(&s_uhi[tp], u);
+    named_sync(1, kTile);
+    const TileInfo ti = tile_info(T, material_of(mstart, p0), material_of(mstart, plast), s_ulo[tp], s_uhi[tp]);
+    if (tid == 0) {  // reset the other slot for the next tile (its last readers passed the barrier above)
       s_ulo[tp ^ 1] = 0xFFFFFFFFu;
       s_uhi[tp ^ 1] = 0;
     }
-    const uint32_t ubase = ulo & ~7u;
-    const uint32_t uend = (uhi + 8) & ~7u;  // exclusive, 16-B multiple
-    const int j0 = T.off[mlo], j1 = T.off[mlo + 1];
-    const bool staged = (mlo == mhi) && (uend - ubase <= (uint32_t)kIgCap) && (j1 > j0);
-    const int cnt = staged ? j1 - j0 : 0;
-
-    if (warp == kTile / 32) {
-      // ---------------------------------------------------------------- producer (one lane)
-      if (lane == 0 && staged) {
-        const uint32_t ig_bytes = (uend - ubase) * 2;
-        int issued = 0, done = 0;
-        while (done < cnt) {
-          while (issued < cnt && issued - done < kStages) {
-            const uint32_t g = it + issued, s = g % kStages, ph = (g / kStages) & 1u;
-            if (!mbar_test(&empty[s], ph ^ 1u)) break;
-            unsigned char *st = stages + (size_t)s * kStageBytes;
-            mbar_arrive_tx(&full_ig[s], ig_bytes);
-            bulk_g2s(st, X.IG + T.ent[j0 + issued].y + ubase, ig_bytes, &full_ig[s]);
-            issued++;
-          }
-          if (issued == done) continue;  // every stage busy: poll again
-          const uint32_t g = it + done, s = g % kStages, ph = (g / kStages) & 1u;
-          if (!mbar_test(&full_ig[s], ph)) continue;
-          unsigned char *st = stages + (size_t)s * kStageBytes;
-          const uint16_t *ig = reinterpret_cast<const uint16_t *>(st);
-          const int klo = ig[ulo - ubase], khi = ig[uhi - ubase];
-          const int nrec = min(khi + 2 - klo, kRecCap);
-          const uint32_t rec0 = T.ent[j0 + done].x + (uint32_t)klo;
-          const uint32_t rdlo = rec0 & ~1u;
-          const uint32_t rdn = (rec0 + (uint32_t)nrec - rdlo + 1u) & ~1u;
-          StageMeta *meta = reinterpret_cast<StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
-          meta->k_lo = klo;
-          meta->n_rec = nrec;
-          meta->rd_lo = rdlo;
-          mbar_arrive_tx(&full[s], (uint32_t)nrec * 48u + (FAST ? rdn * 8u : 0u));
-          bulk_g2s(st + 2 * kIgCap, X.G + (size_t)rec0 * 6, (uint32_t)nrec * 48u, &full[s]);
-          if (FAST) bulk_g2s(st + 2 * kIgCap + 48 * kRecCap, X.Rd + rdlo, rdn * 8u, &full[s]);
-          done++;
+    double m[5];
+#pragma unroll
+    for (int c = 0; c < 5; c++) m[c] = 0.0;
+    const bool fast = FAST && fabs(E) <= 2.0;
+    if (ti.staged) {
+      const uint32_t urel = u - ti.ubase;
+      for (int q = 0; q < ti.cnt; q++) {
+        const uint32_t g = it + q, s = g % kStages, ph = (g / kStages) & 1u;
+        const unsigned char *st = stages + (size_t)s * kStageBytes;
+        mbar_wait(&full[s], ph);
+        const StageMeta meta = *reinterpret_cast<const StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
+        const uint32_t k = reinterpret_cast<const uint16_t *>(st)[urel];
+        const int rel = (int)k - meta.k_lo;
+        const uint2 e = T.ent[ti.j0 + q];
+        Pair P;
+        if (rel + 1 < meta.n_rec) {
+          const double2 *r = reinterpret_cast<const double2 *>(st + 2 * kIgCap) + rel * 3;
+          P.l0 = r[0]; P.l1 = r[1]; P.l2 = r[2]; P.h0 = r[3]; P.h1 = r[4]; P.h2 = r[5];
+          if (FAST) P.y = reinterpret_cast<const double *>(st + 2 * kIgCap + 48 * kRecCap)[e.x + k - meta.rd_lo];
+        } else {
+          load_pair<FAST>(X, e.x + k, P);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (fast)
+          accumulate<true>(P, E, T.conc[ti.j0 + q], m);
+        else
+          accumulate<false>(P, E, T.conc[ti.j0 + q], m);
       }
-      __syncwarp();
+      it += (uint32_t)ti.cnt;
     } else {
-      // ---------------------------------------------------------------- consumers
-      double m[5];
-#pragma unroll
-      for (int c = 0; c < 5; c++) m[c] = 0.0;
-      const bool fast = FAST && fabs(E) <= 2.0;
-      if (staged) {
-        const uint32_t urel = u - ubase;
-        for (int q = 0; q < cnt; q++) {
-          const uint32_t g = it + q, s = g % kStages, ph = (g / kStages) & 1u;
-          const unsigned char *st = stages + (size_t)s * kStageBytes;
-          mbar_wait(&full_ig[s], ph);
-          mbar_wait(&full[s], ph);
-          const StageMeta meta = *reinterpret_cast<const StageMeta *>(st + 2 * kIgCap + 48 * kRecCap + 8 * kRdCap);
-          const uint32_t k = reinterpret_cast<const uint16_t *>(st)[urel];
-          const int rel = (int)k - meta.k_lo;
-          const uint2 e = T.ent[j0 + q];
-          Pair P;
-          if (rel + 1 < meta.n_rec) {
-            const double2 *r = reinterpret_cast<const double2 *>(st + 2 * kIgCap) + rel * 3;
-            P.l0 = r[0]; P.l1 = r[1]; P.l2 = r[2]; P.h0 = r[3]; P.h1 = r[4]; P.h2 = r[5];
-            if (FAST) P.y = reinterpret_cast<const double *>(st + 2 * kIgCap + 48 * kRecCap)[e.x + k - meta.rd_lo];
-          } else {
-            load_pair<FAST>(X, e.x + k, P);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-          if (fast)
-            accumulate<true>(P, E, T.conc[j0 + q], m);
-          else
-            accumulate<false>(P, E, T.conc[j0 + q], m);
-        }
-      } else if (mat >= 0) {
-        const int a0 = T.off[mat], a1 = T.off[mat + 1];
-        if (a1 > a0) {
-          if (fast)
-            nuclide_loop<GF_GRID_UNIONIZED, true, false>(X, T, E, u, a0, a1, m);
-          else
-            nuclide_loop<GF_GRID_UNIONIZED, false, false>(X, T, E, u, a0, a1, m);
-        }
-      }
-      if (p < n) {
-        vacc += argmax5_plus1(m);
-        if (macro_out) {
-          const size_t o = (size_t)idx[p] * 5;
-#pragma unroll
-          for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
-        }
+      const int a0 = T.off[mat], a1 = T.off[mat + 1];
+      if (a1 > a0) {
+        if (fast)
+          nuclide_loop<GF_GRID_UNIONIZED, true, false>(X, T, E, u, a0, a1, m);
+        else
+          nuclide_loop<GF_GRID_UNIONIZED, false, false>(X, T, E, u, a0, a1, m);
       }
     }
-    it += (uint32_t)cnt;
-    if (tid == 0) {
-      s_mlo[tp ^ 1] = -1;
-      s_mhi[tp ^ 1] = -1;
+    if (p < n) {
+      vacc += argmax5_plus1(m);
+      if (macro_out) {
+        const size_t o = (size_t)idx[p] * 5;
+#pragma unroll
+        for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
+      }
     }
-    named_sync(1, kStagedThreads);  // the next tile reuses the other slot; keep the warps in step
   }
   hash_epilogue(vacc, vsum);
 }

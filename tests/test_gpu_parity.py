@@ -205,6 +205,23 @@ def test_C2_small_unionized(gf):
     assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
 
 
+def test_per_thread_sorted_kernel_matches(gf, tmp_path):
+    """GF_XS_STAGED=0 selects the per-thread pipelined kernel for the sorted unionized path; it must
+    give the same bits as the oracle too (run in a child process: the switch is read once)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle as O, paper_2306_11686_b200 as gf\n"
+        "o = O.XSOracle(355, 11303, O.UNIONIZED); g = gf.Grid(gf.Params.xsbench(355, 11303, gf.UNIONIZED))\n"
+        "r1, m1 = o.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
+        "r2, m2 = g.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
+        "assert r1 == r2 and np.array_equal(m1, m2.cpu().numpy())\n"
+        "print('ok')\n")
+    env = dict(os.environ, GF_XS_STAGED="0", PYTHONPATH=os.path.dirname(HERE))
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
+
+
 def test_small_hash_grid(gf):
     o, g = make_pair(gf, 68, 11303, O.HASH)
     check_arrays(o, g)

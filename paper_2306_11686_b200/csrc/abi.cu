@@ -385,7 +385,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 
 // ------------------------------------------------------------------------------------------ lookups
 struct BatchLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, h_macro, h_vsum, h_E, h_mat, total;
+  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, h_macro, h_vsum, h_E, h_mat, total;
 };
 
 static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
@@ -405,6 +405,8 @@ static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool wan
     B.mstart = take(sizeof(uint32_t) * 16);
     B.Es = take(sizeof(double) * n);
     B.idx = take(sizeof(uint32_t) * n);
+    B.us = take(sizeof(uint32_t) * n);
+    B.tinfo = take(32 * ((n + 127) / 128));
   }
   if (flags & GF_HOST_IO) {
     if (want_macro) B.h_macro = take(sizeof(double) * ch * n);
@@ -472,6 +474,8 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
     S.mstart = reinterpret_cast<uint32_t *>(sc + B.mstart);
     S.Es = reinterpret_cast<double *>(sc + B.Es);
     S.idx = reinterpret_cast<uint32_t *>(sc + B.idx);
+    S.us = reinterpret_cast<uint32_t *>(sc + B.us);
+    S.tinfo = sc + B.tinfo;
   }
   cudaEvent_t ev_mid = ev ? static_cast<cudaEvent_t>(ev->before_lookup) : nullptr;
   if (ev && ev->before_sort) GF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev->before_sort), st));

@@ -464,25 +464,13 @@ inline size_t staged_smem(int total) {
   return t + (size_t)kStages * kStageBytes;
 }
 
-// Tile facts both sides derive identically: material of the first / last lookup and the index
-// range [energy_index(min E), energy_index(max E)] (energy_index is monotone in E).
+// Tile facts (per kTile sorted lookups), computed by staged_prep and read by both the producer and
+// the consumers of xs_lookup_staged: the material of the first lookup, the unionized index range
+// [min u, max u] of the tile (16-B aligned base) and whether the tile is staged.
 struct TileInfo {
-  int staged, j0, cnt;
-  uint32_t ubase, ulo, uhi;
+  int staged, j0, cnt, mat;
+  uint32_t ubase, ulo, uhi, pad;
 };
-
-__device__ __forceinline__ TileInfo tile_info(const XsTables &T, int mlo, int mhi, uint32_t ulo, uint32_t uhi) {
-  TileInfo t;
-  t.ubase = ulo & ~7u;
-  t.ulo = ulo;
-  t.uhi = uhi;
-  const uint32_t uend = (uhi + 8) & ~7u;
-  t.j0 = T.off[mlo];
-  const int j1 = T.off[mlo + 1];
-  t.staged = (mlo == mhi) && (uend - t.ubase <= (uint32_t)kIgCap) && (j1 > t.j0);
-  t.cnt = t.staged ? j1 - t.j0 : 0;
-  return t;
-}
 
 __device__ __forceinline__ int material_of(const uint32_t *mstart, uint32_t p) {
   int mat = 0;
@@ -492,9 +480,57 @@ __device__ __forceinline__ int material_of(const uint32_t *mstart, uint32_t p) {
   return mat;
 }
 
+// One CTA of kTile threads per tile: us[p] = the unionized index of the sorted lookup p (A3, the
+// same two-level search as every other kernel), and the tile's facts.  Massively parallel, so the
+// dependent search latency is hidden here instead of inside the staged kernel.
+__global__ void __launch_bounds__(kTile) staged_prep(XsDev X, uint32_t n, const double *__restrict__ Es,
+                                                     const uint32_t *__restrict__ mstart, uint32_t *__restrict__ us,
+                                                     TileInfo *__restrict__ tinfo) {
+  __shared__ uint32_t s_lo[kTile / 32], s_hi[kTile / 32];
+  const uint32_t tile = blockIdx.x, p0 = tile * kTile, plast = min(n, p0 + kTile) - 1;
+  const uint32_t p = p0 + threadIdx.x, pc = min(p, plast);
+  const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, Es[pc]);
+  if (p < n) us[p] = u;
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, u), hi = __reduce_max_sync(0xffffffffu, u);
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[threadIdx.x >> 5] = lo;
+    s_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t ulo = s_lo[0], uhi = s_hi[0];
+    for (int w = 1; w < kTile / 32; w++) {
+      ulo = min(ulo, s_lo[w]);
+      uhi = max(uhi, s_hi[w]);
+    }
+    const int mlo = material_of(mstart, p0), mhi = material_of(mstart, plast);
+    TileInfo t;
+    t.mat = mlo;
+    t.ubase = ulo & ~7u;
+    t.ulo = ulo;
+    t.uhi = uhi;
+    t.pad = 0;
+    const uint32_t uend = (uhi + 8) & ~7u;  // exclusive, 16-B multiple of u16 entries
+    t.j0 = __ldg(X.moff + mlo);
+    const int j1 = __ldg(X.moff + mlo + 1);
+    t.staged = (mlo == mhi) && (uend - t.ubase <= (uint32_t)kIgCap) && (j1 > t.j0);
+    t.cnt = t.staged ? j1 - t.j0 : 0;
+    tinfo[tile] = t;
+  }
+}
+
+__device__ __forceinline__ TileInfo load_tinfo(const TileInfo *t) {
+  const int4 a = __ldg(reinterpret_cast<const int4 *>(t)), b = __ldg(reinterpret_cast<const int4 *>(t) + 1);
+  TileInfo r;
+  r.staged = a.x; r.j0 = a.y; r.cnt = a.z; r.mat = a.w;
+  r.ubase = (uint32_t)b.x; r.ulo = (uint32_t)b.y; r.uhi = (uint32_t)b.z; r.pad = 0;
+  return r;
+}
+
 template <bool FAST>
 __global__ void __launch_bounds__(kStagedThreads, 3)
-    xs_lookup_staged(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ idx,
+    xs_lookup_staged(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ us,
+                     const TileInfo *__restrict__ tinfo, const uint32_t *__restrict__ idx,
                      const uint32_t *__restrict__ mstart, double *__restrict__ macro_out,
                      unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -505,8 +541,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   uint64_t *empty = full + kStages;
   off = (off + 3 * kStages * 8 + 127) & ~size_t(127);
   unsigned char *stages = smem + off;
-  __shared__ uint32_t s_ulo[2], s_uhi[2];
-  __shared__ TileInfo s_ring[kStages];  // producer-private: tile facts of in-flight items
+  __shared__ TileInfo s_ring[kStages];  // producer-private: facts of the staged tiles in flight
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -517,42 +552,22 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < 2) {
-    s_ulo[tid] = 0xFFFFFFFFu;
-    s_uhi[tid] = 0;
-  }
   __syncthreads();
   const uint32_t ntiles = (n + kTile - 1) / kTile;
 
   if (warp == kTile / 32) {
     // ================================================================ producer warp
     // Walks the CTA's tiles in the consumers' order; cursor A issues index-grid segments up to
-    // kLook items ahead of cursor B, which issues record ranges once a segment has landed.  All
-    // lanes run the control flow (tile facts are a warp reduction); lane 0 issues.
+    // kLook items ahead of cursor B, which issues the record ranges once a segment has landed.
+    // All lanes run the control flow; lane 0 issues.
     constexpr int kLook = kStages - 2;
-    uint32_t tA = blockIdx.x;                   // tile of cursor A
-    int qA = 0, qB = 0;                         // item within the tile
-    uint32_t gA = 0, gB = 0;                    // global item counters
-    TileInfo iA{0, 0, 0, 0, 0, 0}, iB{0, 0, 0, 0, 0, 0};
+    uint32_t tA = blockIdx.x;  // tile of cursor A
+    int qA = 0, qB = 0;        // item within the tile
+    uint32_t gA = 0, gB = 0;   // global item counters (ring positions)
+    TileInfo iA{}, iB{};
+    TileInfo preA = load_tinfo(tinfo + min(tA, ntiles - 1));  // tile facts one tile ahead
     bool haveA = false, haveB = false;
-    uint32_t ringA = 0, ringB = 0;  // tile-info ring slots (tiles entered by A / B)
-    auto info_of = [&](uint32_t tile) {
-      const uint32_t p0 = tile * kTile, plast = min(n, p0 + kTile) - 1;
-      double lo = 3.0e300, hi = -3.0e300;
-      for (uint32_t p = p0 + lane; p <= plast; p += 32) {
-        const double e = Es[p];
-        lo = fmin(lo, e);
-        hi = fmax(hi, e);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      const uint32_t ulo = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, lo);
-      const uint32_t uhi = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, hi);
-      return tile_info(T, material_of(mstart, p0), material_of(mstart, plast), ulo, uhi);
-    };
+    uint32_t ringA = 0, ringB = 0;
     // Advance a cursor to its next staged item; false at the end of the CTA's tiles.  Only staged
     // tiles enter the ring, so it holds at most kLook + 1 <= kStages tiles between B and A.
     auto advanceA = [&]() -> bool {
@@ -560,7 +575,8 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
         if (haveA && qA < iA.cnt) return true;
         if (haveA) tA += gridDim.x;
         if (tA >= ntiles) return false;
-        iA = info_of(tA);
+        iA = preA;
+        if (tA + gridDim.x < ntiles) preA = load_tinfo(tinfo + tA + gridDim.x);
         haveA = true;
         qA = 0;
         if (iA.cnt > 0) {
@@ -626,22 +642,13 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   // ================================================================== consumer warps
   uint32_t it = 0;  // staged items consumed so far (ring position)
   uint32_t vacc = 0;
-  int tp = 0;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tp ^= 1) {
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t p0 = tile * kTile;
     const uint32_t plast = min(n, p0 + kTile) - 1;
     const uint32_t p = p0 + tid, pc = min(p, plast);
-    const int mat = material_of(mstart, pc);
+    const TileInfo ti = load_tinfo(tinfo + tile);
     const double E = Es[pc];
-    const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
-    atomicMin(&s_ulo[tp], u);
-    atomicMax(&s_uhi[tp], u);
-    named_sync(1, kTile);
-    const TileInfo ti = tile_info(T, material_of(mstart, p0), material_of(mstart, plast), s_ulo[tp], s_uhi[tp]);
-    if (tid == 0) {  // reset the other slot for the next tile (its last readers passed the barrier above)
-      s_ulo[tp ^ 1] = 0xFFFFFFFFu;
-      s_uhi[tp ^ 1] = 0;
-    }
+    const uint32_t u = us[pc];
     double m[5];
 #pragma unroll
     for (int c = 0; c < 5; c++) m[c] = 0.0;
@@ -673,6 +680,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
       }
       it += (uint32_t)ti.cnt;
     } else {
+      const int mat = material_of(mstart, pc);
       const int a0 = T.off[mat], a1 = T.off[mat + 1];
       if (a1 > a0) {
         if (fast)
@@ -713,8 +721,12 @@ static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t ntiles = (n + kTile - 1) / kTile;
+  TileInfo *tinfo = reinterpret_cast<TileInfo *>(S.tinfo);
+  staged_prep<<<ntiles, kTile, 0, st>>>(X, n, S.Es, S.mstart, S.us, tinfo);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm[FAST], 1)));
-  xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
+  xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.us, tinfo, S.idx, S.mstart, macro_out,
+                                                             vsum);
   return cudaGetLastError();
 }
 

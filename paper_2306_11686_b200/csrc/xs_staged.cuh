@@ -1,44 +1,27 @@
-// xs_staged.cuh -- the sorted unionized lookup with its memory side on the TMA engine.
+// xs_staged.cuh -- the sorted unionized lookup with the index-grid stream on the TMA engine.
 // Included by xs_lookup.cu (uses its XsTables / Pair / accumulate / nuclide_loop / energy_index).
 //
 // Persistent CTAs of 4 consumer warps + 1 producer warp walk tiles of kTile consecutive sorted
 // lookups.  staged_prep (a separate, massively parallel pass) computes each sorted lookup's
 // unionized index u and each tile's facts: material of its first / last lookup and [min u, max u].
 // A tile whose lookups share one material and whose u range spans <= kIgCap entries is "staged":
-// for each nuclide j of the material the producer warp
-//   cursor A: issues cp.async.bulk of the tile's index-grid row segment IG[nuc][u_lo..u_hi] into
-//             SMEM stage s (mbarrier full_ig[s]), up to kLook items ahead of cursor B;
-//   cursor B: once that segment has landed, reads k_lo = IG[u_lo], k_hi = IG[u_hi] (the index grid
-//             is monotone in u) and issues cp.async.bulk of the record range [k_lo, k_hi + 1] of the
-//             nuclide grid and of the matching reciprocal widths (mbarrier full[s]).
-// Stages form a ring of kStages guarded by empty[s] (one arrival per consumer warp).  Consumers
-// read their interval index, record pair and reciprocal width from SMEM -- no global access in the
-// inner loop; records past kRecCap (rare) fall back to global loads.  Other tiles (mixed
-// material, sparse materials whose u range is wide, caller energies outside [-2, 2]) run the
+// for each nuclide j of the material the producer lane issues one cp.async.bulk of the tile's
+// index-grid row segment IG[nuc][u_lo..u_hi] into SMEM stage s of a kStages ring (mbarrier full[s]
+// completes on the transaction count; empty[s] takes one arrival per consumer warp).  The producer
+// has no dependent work, so the ring runs kStages items ahead of the consumers and the DRAM
+// latency of the index grid (the one structure this path streams from HBM) is hidden.  Consumers
+// read their interval index k from SMEM, release the stage at once, and load the 96-B record pair
+// (and reciprocal width) with one item of lookahead -- sorted neighbours share records, so these
+// hit L1/L2.  Other tiles (mixed material, sparse materials whose u range is wide) run the
 // per-thread pipelined loop.  Results are bit-identical to every other kernel: same index, same
 // arithmetic, same order.
 #pragma once
 
 constexpr int kTile = 128;                   // lookups per tile = consumer threads
 constexpr int kStagedThreads = kTile + 32;   // + producer warp
-constexpr int kStages = 24;                  // ring depth
-constexpr int kLook = kStages - 2;           // cursor A runs at most kLook items ahead of cursor B
+constexpr int kStages = 24;                  // ring depth (items of lookahead)
 constexpr int kIgCap = 1024;                 // index-grid entries per stage (2 KB)
-constexpr int kRecCap = 8;                   // records per stage (k_hi - k_lo + 2 <= 8: >99.9%)
-constexpr int kRdCap = kRecCap + 2;          // reciprocal widths per stage (range rounded to 16 B)
-// stage layout: ig[kIgCap] u16 | rec[kRecCap] 48-B records | rd[kRdCap] f64 | StageMeta (16 B)
-constexpr int kRecOff = 2 * kIgCap;
-constexpr int kRdOff = kRecOff + 48 * kRecCap;
-constexpr int kMetaOff = kRdOff + 8 * kRdCap;
-constexpr int kStageBytes = (kMetaOff + 16 + 127) & ~127;
-static_assert(kRecOff % 16 == 0 && kRdOff % 16 == 0 && kMetaOff % 16 == 0, "bulk-copy targets are 16-B aligned");
-
-struct StageMeta {
-  int k_lo;        // record index (within the nuclide) of rec[0]
-  int n_rec;       // records staged
-  uint32_t rd_lo;  // absolute index (into Rd) of rd[0]
-  int pad;
-};
+constexpr int kStageBytes = 2 * kIgCap;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -67,7 +50,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 inline size_t staged_smem(int total) {
   size_t t = (xs_table_smem(total) + 15) & ~size_t(15);
-  t += 3 * kStages * 8;
+  t += 2 * kStages * 8;
   t = (t + 127) & ~size_t(127);
   return t + (size_t)kStages * kStageBytes;
 }
@@ -98,7 +81,7 @@ __global__ void __launch_bounds__(kTile) staged_prep(XsDev X, uint32_t n, const 
   const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
   if (p < n) us[p] = u;
   const uint32_t lo = __reduce_min_sync(0xffffffffu, u), hi = __reduce_max_sync(0xffffffffu, u);
-  // caller-supplied energies outside [-2, 2] need the IEEE division path: such tiles are not staged
+  // energies outside [-2, 2] (caller-supplied only) need the IEEE division path: not staged
   const int odd = __syncthreads_or(!(fabs(E) <= 2.0));
   if ((threadIdx.x & 31) == 0) {
     s_lo[threadIdx.x >> 5] = lo;
@@ -141,31 +124,34 @@ __device__ __forceinline__ TileInfo load_tinfo(const TileInfo *t) {
   return r;
 }
 
-// Consumer side of one staged item: wait for stage g, read k and the record pair (SMEM, or global
-// past kRecCap), release the stage (one arrival per warp).
+// Consumer side of one staged item: wait for stage g, read k, release the stage (one arrival per
+// warp), issue the record-pair loads.
 template <bool FAST>
 __device__ __forceinline__ void staged_fetch(const XsDev &X, unsigned char *stages, uint64_t *full, uint64_t *empty,
                                              uint32_t g, uint32_t urel, uint32_t rec_base, int lane, Pair &P) {
   const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-  const unsigned char *st = stages + (size_t)s * kStageBytes;
   mbar_wait(&full[s], ph);
-  const StageMeta meta = *reinterpret_cast<const StageMeta *>(st + kMetaOff);
-  const uint32_t k = reinterpret_cast<const uint16_t *>(st)[urel];
-  const int rel = (int)k - meta.k_lo;
-  if (rel + 1 < meta.n_rec) {
-    const double2 *r = reinterpret_cast<const double2 *>(st + kRecOff) + rel * 3;
-    P.l0 = r[0];
-    P.l1 = r[1];
-    P.l2 = r[2];
-    P.h0 = r[3];
-    P.h1 = r[4];
-    P.h2 = r[5];
-    if (FAST) P.y = reinterpret_cast<const double *>(st + kRdOff)[rec_base + k - meta.rd_lo];
-  } else {
-    load_pair<FAST>(X, rec_base + k, P);
-  }
+  const uint32_t k = reinterpret_cast<const uint16_t *>(stages + (size_t)s * kStageBytes)[urel];
   __syncwarp();
   if (lane == 0) mbar_arrive(&empty[s]);
+  load_pair<FAST>(X, rec_base + k, P);
+}
+
+// Look kPeek items ahead in the ring: read that item's interval index from its (landed) stage and
+// prefetch its record pair and reciprocal width into L1, so the loads of staged_fetch hit.
+constexpr int kPeek = 4;
+static_assert(kPeek + 2 < kStages, "the peeked stage must still be held by the consumers");
+
+template <bool FAST>
+__device__ __forceinline__ void staged_peek(const XsDev &X, unsigned char *stages, uint64_t *full, uint32_t g,
+                                            uint32_t urel, uint32_t rec_base) {
+  const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
+  mbar_wait(&full[s], ph);
+  const uint32_t k = reinterpret_cast<const uint16_t *>(stages + (size_t)s * kStageBytes)[urel];
+  const char *a = reinterpret_cast<const char *>(X.G + (size_t)(rec_base + k) * 6);
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 88));
+  if (FAST) asm volatile("prefetch.global.L1 [%0];" ::"l"(X.Rd + rec_base + k));
 }
 
 // Staged tiles only hold energies in [-2, 2] (staged_prep), so FAST needs no per-lookup check.
@@ -173,11 +159,19 @@ template <bool FAST>
 __device__ __forceinline__ void staged_loop(const XsDev &X, const XsTables &T, unsigned char *stages, uint64_t *full,
                                             uint64_t *empty, uint32_t it, const TileInfo &ti, uint32_t urel,
                                             double E, int lane, double m[5]) {
+  Pair A, B;
   const int j0 = ti.j0, cnt = ti.cnt;
-  for (int q = 0; q < cnt; q++) {
-    Pair P;
-    staged_fetch<FAST>(X, stages, full, empty, it + q, urel, T.ent[j0 + q].x, lane, P);
-    accumulate<FAST>(P, E, T.conc[j0 + q], m);
+  for (int q = 0; q < kPeek && q < cnt; q++) staged_peek<FAST>(X, stages, full, it + q, urel, T.ent[j0 + q].x);
+  staged_fetch<FAST>(X, stages, full, empty, it, urel, T.ent[j0].x, lane, A);
+  for (int q = 0; q < cnt; q += 2) {
+    if (q + kPeek < cnt) staged_peek<FAST>(X, stages, full, it + q + kPeek, urel, T.ent[j0 + q + kPeek].x);
+    if (q + 1 + kPeek < cnt)
+      staged_peek<FAST>(X, stages, full, it + q + 1 + kPeek, urel, T.ent[j0 + q + 1 + kPeek].x);
+    if (q + 1 < cnt) staged_fetch<FAST>(X, stages, full, empty, it + q + 1, urel, T.ent[j0 + q + 1].x, lane, B);
+    accumulate<FAST>(A, E, T.conc[j0 + q], m);
+    if (q + 1 >= cnt) break;
+    if (q + 2 < cnt) staged_fetch<FAST>(X, stages, full, empty, it + q + 2, urel, T.ent[j0 + q + 2].x, lane, A);
+    accumulate<FAST>(B, E, T.conc[j0 + q + 1], m);
   }
 }
 
@@ -190,17 +184,14 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
   size_t off = (xs_table_smem(X.total) + 15) & ~size_t(15);
-  uint64_t *full_ig = reinterpret_cast<uint64_t *>(smem + off);
-  uint64_t *full = full_ig + kStages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + off);
   uint64_t *empty = full + kStages;
-  off = (off + 3 * kStages * 8 + 127) & ~size_t(127);
+  off = (off + 2 * kStages * 8 + 127) & ~size_t(127);
   unsigned char *stages = smem + off;
-  __shared__ TileInfo s_ring[kStages];  // producer-private: facts of the staged tiles in flight
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
-      mbar_init(&full_ig[s], 1);
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTile / 32);
     }
@@ -210,82 +201,23 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
   const uint32_t ntiles = (n + kTile - 1) / kTile;
 
   if (warp == kTile / 32) {
-    // ================================================================ producer warp
-    // All lanes run the control flow; lane 0 issues.
-    uint32_t tA = blockIdx.x;  // tile of cursor A
-    int qA = 0, qB = 0;        // item within the tile
-    uint32_t gA = 0, gB = 0;   // global item counters (ring positions)
-    TileInfo iA{}, iB{};
-    TileInfo preA = load_tinfo(tinfo + min(tA, ntiles - 1));  // tile facts one tile ahead
-    bool haveA = false, haveB = false;
-    uint32_t ringA = 0, ringB = 0;
-    // Advance a cursor to its next staged item; false at the end of the CTA's tiles.  Only staged
-    // tiles enter the ring, so it holds at most kLook + 1 <= kStages tiles between B and A.
-    auto advanceA = [&]() -> bool {
-      while (true) {
-        if (haveA && qA < iA.cnt) return true;
-        if (haveA) tA += gridDim.x;
-        if (tA >= ntiles) return false;
-        iA = preA;
-        if (tA + gridDim.x < ntiles) preA = load_tinfo(tinfo + tA + gridDim.x);
-        haveA = true;
-        qA = 0;
-        if (iA.cnt > 0) {
-          if (lane == 0) s_ring[ringA % kStages] = iA;
-          ringA++;
-        }
-      }
-    };
-    auto advanceB = [&]() -> bool {
-      if (haveB && qB < iB.cnt) return true;
-      if (ringB == ringA) return false;
-      __syncwarp();
-      iB = s_ring[ringB % kStages];
-      ringB++;
-      haveB = true;
-      qB = 0;
-      return true;
-    };
-    bool moreA = advanceA();
-    while (true) {
-      // cursor A: index-grid segments, at most kLook items ahead of B
-      while (moreA && gA < gB + kLook) {
-        const uint32_t s = gA % kStages, ph = (gA / kStages) & 1u;
+    // ================================================================ producer warp (lane 0 issues)
+    uint32_t g = 0;
+    TileInfo nxt = load_tinfo(tinfo + min((uint32_t)blockIdx.x, ntiles - 1));
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = nxt;
+      if (tile + gridDim.x < ntiles) nxt = load_tinfo(tinfo + tile + gridDim.x);  // one tile ahead
+      if (!ti.staged) continue;
+      const uint32_t bytes = (((ti.uhi + 8) & ~7u) - ti.ubase) * 2;
+      for (int q = 0; q < ti.cnt; q++, g++) {
+        const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         if (lane == 0) {
-          const uint32_t bytes = (((iA.uhi + 8) & ~7u) - iA.ubase) * 2;
-          mbar_arrive_tx(&full_ig[s], bytes);
-          bulk_g2s(stages + (size_t)s * kStageBytes, X.IG + T.ent[iA.j0 + qA].y + iA.ubase, bytes, &full_ig[s]);
+          mbar_arrive_tx(&full[s], bytes);
+          bulk_g2s(stages + (size_t)s * kStageBytes, X.IG + T.ent[ti.j0 + q].y + ti.ubase, bytes, &full[s]);
         }
         __syncwarp();
-        gA++;
-        qA++;
-        moreA = advanceA();
       }
-      if (gB == gA) break;  // A exhausted and B caught up
-      if (!advanceB()) break;
-      // cursor B: record range of item gB once its index-grid segment has landed
-      const uint32_t s = gB % kStages, ph = (gB / kStages) & 1u;
-      mbar_wait(&full_ig[s], ph);
-      if (lane == 0) {
-        unsigned char *st = stages + (size_t)s * kStageBytes;
-        const uint16_t *ig = reinterpret_cast<const uint16_t *>(st);
-        const int klo = ig[iB.ulo - iB.ubase], khi = ig[iB.uhi - iB.ubase];
-        const int nrec = min(khi + 2 - klo, kRecCap);
-        const uint32_t rec0 = T.ent[iB.j0 + qB].x + (uint32_t)klo;
-        const uint32_t rdlo = rec0 & ~1u;
-        const uint32_t rdn = (rec0 + (uint32_t)nrec - rdlo + 1u) & ~1u;
-        StageMeta *meta = reinterpret_cast<StageMeta *>(st + kMetaOff);
-        meta->k_lo = klo;
-        meta->n_rec = nrec;
-        meta->rd_lo = rdlo;
-        mbar_arrive_tx(&full[s], (uint32_t)nrec * 48u + (FAST ? rdn * 8u : 0u));
-        bulk_g2s(st + kRecOff, X.G + (size_t)rec0 * 6, (uint32_t)nrec * 48u, &full[s]);
-        if (FAST) bulk_g2s(st + kRdOff, X.Rd + rdlo, rdn * 8u, &full[s]);
-      }
-      __syncwarp();
-      gB++;
-      qB++;
     }
     hash_epilogue(0u, vsum);
     return;
@@ -304,6 +236,7 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
     double m[5];
 #pragma unroll
     for (int c = 0; c < 5; c++) m[c] = 0.0;
+    const bool fast = FAST && fabs(E) <= 2.0;
     if (ti.staged) {
       staged_loop<FAST>(X, T, stages, full, empty, it, ti, u - ti.ubase, E, lane, m);
       it += (uint32_t)ti.cnt;
@@ -311,8 +244,8 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
       const int mat = material_of(mstart, pc);
       const int a0 = T.off[mat], a1 = T.off[mat + 1];
       if (a1 > a0) {
-        if (FAST && fabs(E) <= 2.0)
-          nuclide_loop<GF_GRID_UNIONIZED, FAST, false>(X, T, E, u, a0, a1, m);
+        if (fast)
+          nuclide_loop<GF_GRID_UNIONIZED, true, false>(X, T, E, u, a0, a1, m);
         else
           nuclide_loop<GF_GRID_UNIONIZED, false, false>(X, T, E, u, a0, a1, m);
       }

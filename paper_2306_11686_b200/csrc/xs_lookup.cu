@@ -389,15 +389,22 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 // ------------------------------------------------------------------------------------------ staged
 #include "xs_staged.cuh"
 
-// GF_XS_STAGED=0 in the environment selects the per-thread kernel for the sorted unionized path
-// (A/B measurements); the default is the staged kernel.
-static bool use_staged() {
+// ------------------------------------------------------------------------------------------ production
+#include "xs_sorted_u.cuh"
+
+// Kernel for the sorted unionized path.  GF_XS_KERNEL in the environment selects an alternative for
+// A/B measurements: "staged" (TMA producer/consumer ring), "thread" (non-persistent per-thread
+// kernel); default "ring" (persistent, register-ring lookahead).  All give identical results.
+enum { kKernRing = 0, kKernStaged = 1, kKernThread = 2 };
+static int sorted_u_kernel() {
   static int v = -1;
   if (v < 0) {
-    const char *s = getenv("GF_XS_STAGED");
-    v = (s && s[0] == '0') ? 0 : 1;
+    const char *s = getenv("GF_XS_KERNEL");
+    v = kKernRing;
+    if (s && s[0] == 's') v = kKernStaged;
+    if (s && s[0] == 't') v = kKernThread;
   }
-  return v == 1;
+  return v;
 }
 
 template <int GT>
@@ -410,9 +417,12 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, macro_out != nullptr, st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    if (GT == GF_GRID_UNIONIZED && use_staged())
+    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernStaged)
       return X.fastdiv ? launch_staged<true>(X, n, S, macro_out, vsum, st)
                        : launch_staged<false>(X, n, S, macro_out, vsum, st);
+    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernRing)
+      return X.fastdiv ? launch_sorted_u<true>(X, n, S, macro_out, vsum, st)
+                       : launch_sorted_u<false>(X, n, S, macro_out, vsum, st);
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;

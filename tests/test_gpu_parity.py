@@ -205,9 +205,11 @@ def test_C2_small_unionized(gf):
     assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
 
 
-def test_per_thread_sorted_kernel_matches(gf, tmp_path):
-    """GF_XS_STAGED=0 selects the per-thread pipelined kernel for the sorted unionized path; it must
-    give the same bits as the oracle too (run in a child process: the switch is read once)."""
+@pytest.mark.parametrize("kernel", ["staged", "thread"])
+def test_alternative_sorted_kernels_match(gf, kernel):
+    """GF_XS_KERNEL selects the alternative kernels of the sorted unionized path (the TMA-staged
+    producer/consumer ring, the non-persistent per-thread kernel); they must give the oracle's bits
+    too (run in a child process: the switch is read once)."""
     import subprocess
     import sys
     code = (
@@ -217,7 +219,7 @@ def test_per_thread_sorted_kernel_matches(gf, tmp_path):
         "r2, m2 = g.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
         "assert r1 == r2 and np.array_equal(m1, m2.cpu().numpy())\n"
         "print('ok')\n")
-    env = dict(os.environ, GF_XS_STAGED="0", PYTHONPATH=os.path.dirname(HERE))
+    env = dict(os.environ, GF_XS_KERNEL=kernel, PYTHONPATH=os.path.dirname(HERE))
     res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
 

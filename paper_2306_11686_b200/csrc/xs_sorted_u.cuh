@@ -11,7 +11,15 @@
 // The loop body is unrolled by kDepth so the register ring is statically indexed.
 #pragma once
 
-constexpr int kDepth = 8;  // index-grid lookahead (nuclides)
+constexpr int kDepth = 8;   // index-grid lookahead (nuclides)
+constexpr int kPairPf = 3;  // record-pair L1 prefetch lookahead (nuclides), < kDepth
+
+// A3 for every sorted lookup in a separate, massively parallel pass: us[p] = u of lookup p.
+__global__ void __launch_bounds__(256) us_prep(XsDev X, uint32_t n, const double *__restrict__ Es,
+                                               uint32_t *__restrict__ us) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) us[p] = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, Es[p]);
+}
 
 template <bool FAST>
 __device__ __forceinline__ void unionized_loop(const XsDev &X, const XsTables &T, double E, uint32_t u, int j0, int j1,
@@ -28,6 +36,13 @@ __device__ __forceinline__ void unionized_loop(const XsDev &X, const XsTables &T
       if (jj >= j1) break;
       Pair &cur = (i & 1) ? B : A;
       Pair &nxt = (i & 1) ? A : B;
+      if (jj + kPairPf < j1) {  // L1 prefetch of the pair (and reciprocal) kPairPf nuclides ahead
+        const uint32_t rec = T.ent[jj + kPairPf].x + kq[(i + kPairPf) % kDepth];
+        const char *a = reinterpret_cast<const char *>(X.G + (size_t)rec * 6);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 88));
+        if (FAST) asm volatile("prefetch.global.L1 [%0];" ::"l"(X.Rd + rec));
+      }
       if (jj + 1 < j1) load_pair<FAST>(X, T.ent[jj + 1].x + kq[(i + 1) % kDepth], nxt);
       if (jj + kDepth < j1) kq[i] = (uint32_t)__ldg(X.IG + T.ent[jj + kDepth].y + u);
       accumulate<FAST>(cur, E, T.conc[jj], m);
@@ -37,8 +52,8 @@ __device__ __forceinline__ void unionized_loop(const XsDev &X, const XsTables &T
 
 template <bool FAST>
 __global__ void __launch_bounds__(kLookupTpb, 4)
-    xs_lookup_sorted_u(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ idx,
-                       const uint32_t *__restrict__ mstart, double *__restrict__ macro_out,
+    xs_lookup_sorted_u(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ us,
+                       const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart, double *__restrict__ macro_out,
                        unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
@@ -55,7 +70,7 @@ __global__ void __launch_bounds__(kLookupTpb, 4)
     for (int mm = 1; mm < kMats; mm++)
       if (p >= ms[mm]) mat = mm;
     const double E = Es[p];
-    const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
+    const uint32_t u = us[p];
     double m[5];
 #pragma unroll
     for (int c = 0; c < 5; c++) m[c] = 0.0;
@@ -94,6 +109,8 @@ static cudaError_t launch_sorted_u(const XsDev &X, uint32_t n, const SortScratch
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t ntiles = (n + kLookupTpb - 1) / kLookupTpb;
   const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm[FAST], 1)));
-  xs_lookup_sorted_u<FAST><<<grid, kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
+  us_prep<<<nblk(n, 256), 256, 0, st>>>(X, n, S.Es, S.us);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  xs_lookup_sorted_u<FAST><<<grid, kLookupTpb, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, macro_out, vsum);
   return cudaGetLastError();
 }

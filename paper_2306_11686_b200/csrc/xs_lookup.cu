@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
       E = lcg_draw(s);
       mat = pick_material(lcg_draw(s), sT);
     }
-    atomicAdd(counts + mat * kNB + energy_bin(E), 1u);
+    atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
   }
 }
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
       E = lcg_draw(s);
       mat = pick_material(lcg_draw(s), sT);
     }
-    uint32_t pos = atomicAdd(cursor + mat * kNB + energy_bin(E), 1u);
+    uint32_t pos = atomicAdd(cursor + mat * kNB + sort_bin(E), 1u);
     Es[pos] = E;
     if (idx) idx[pos] = (uint32_t)t;
   }
@@ -393,16 +393,18 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 #include "xs_sorted_u.cuh"
 
 // Kernel for the sorted unionized path.  GF_XS_KERNEL in the environment selects an alternative for
-// A/B measurements: "staged" (TMA producer/consumer ring), "thread" (non-persistent per-thread
-// kernel); default "ring" (persistent, register-ring lookahead).  All give identical results.
-enum { kKernRing = 0, kKernStaged = 1, kKernThread = 2 };
+// A/B measurements: "staged" (TMA producer/consumer ring), "thread" (non-persistent, one lookup per
+// thread), "ring" (persistent, one lookup per thread, register-ring lookahead); default "group"
+// (persistent, kL lookups per thread).  All give identical results.
+enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2, kKernRing = 3 };
 static int sorted_u_kernel() {
   static int v = -1;
   if (v < 0) {
     const char *s = getenv("GF_XS_KERNEL");
-    v = kKernRing;
+    v = kKernGroup;
     if (s && s[0] == 's') v = kKernStaged;
     if (s && s[0] == 't') v = kKernThread;
+    if (s && s[0] == 'r') v = kKernRing;
   }
   return v;
 }
@@ -423,6 +425,9 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernRing)
       return X.fastdiv ? launch_sorted_u<true>(X, n, S, macro_out, vsum, st)
                        : launch_sorted_u<false>(X, n, S, macro_out, vsum, st);
+    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernGroup)
+      return X.fastdiv ? launch_sorted_u4<true>(X, n, S, macro_out, vsum, st)
+                       : launch_sorted_u4<false>(X, n, S, macro_out, vsum, st);
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;

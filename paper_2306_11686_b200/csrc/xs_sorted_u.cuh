@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kLookupTpb, 4)
 // thread carries kL independent FP64 chains.  A lookup whose interval differs reloads the pair.
 constexpr int kL = 4;
 constexpr int kTpbL = 128;
+constexpr int kIgPf = 10;  // index-grid L2 prefetch distance (nuclides)
 
 template <bool FAST>
 __device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_base, const uint32_t (&k)[kL], Pair &P,
@@ -118,8 +119,10 @@ __device__ __forceinline__ void load_k(const XsDev &X, uint32_t row, const uint3
   for (int i = 0; i < kL; i++) k[i] = __ldg(X.IG + row + u[i]);
 }
 
-// Nuclides j0..j1-1 for kL lookups: index-grid values 3 nuclides ahead, the pair of lookup 0's
-// interval 1 nuclide ahead (two buffers); unrolled by 4 so the rings are statically indexed.
+// Nuclides j0..j1-1 for kL lookups: index-grid values 3 nuclides ahead (register ring) and kIgPf
+// ahead in L2 (prefetch), the pair of lookup 0's interval 1 nuclide ahead (two buffers); unrolled
+// by 4 so the rings are statically indexed.  (A deeper ring overflows the instruction cache or the
+// register file: measured.)
 template <bool FAST>
 __device__ __forceinline__ void unionized_loop4(const XsDev &X, const XsTables &T, const double (&E)[kL],
                                                 const uint32_t (&u)[kL], int j0, int j1, double (&m)[kL][5]) {
@@ -143,6 +146,8 @@ __device__ __forceinline__ void unionized_loop4(const XsDev &X, const XsTables &
         knxt = kq[(i + 1) & 3][0];
         load_pair<FAST>(X, T.ent[jj + 1].x + knxt, nxt);
       }
+      if (jj + kIgPf < j1)  // index-grid line of nuclide jj + kIgPf into L2 (no register cost)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(X.IG + T.ent[jj + kIgPf].y + u[0]));
       if (jj + 3 < j1) load_k(X, T.ent[jj + 3].y, u, kq[(i + 3) & 3]);
       accumulate_group<FAST>(X, T.ent[jj].x, kq[i], cur, kcur, E, T.conc[jj], m);
     }

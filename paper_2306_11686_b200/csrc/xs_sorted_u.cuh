@@ -160,10 +160,9 @@ __global__ void __launch_bounds__(kTpbL, 3)
                         const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart,
                         double *__restrict__ macro_out, unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const XsTables T = stage_xs_tables(X, smem);
-  uint32_t ms[kMats + 1];
-#pragma unroll
-  for (int mm = 0; mm <= kMats; mm++) ms[mm] = __ldg(mstart + mm);
+  __shared__ uint32_t ms[kMats + 1];  // material segment starts (SMEM: registers go to the loop)
+  if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
+  const XsTables T = stage_xs_tables(X, smem);  // (its __syncthreads also publishes ms)
   uint32_t vacc = 0;
   const uint32_t ngroups = (n + kL - 1) / kL;
   for (uint32_t g = blockIdx.x * kTpbL + threadIdx.x; g < ngroups; g += gridDim.x * kTpbL) {

@@ -37,7 +37,26 @@ CONFIGS = {
 }
 # Per-lookup algorithmic work of the dominant kernel:
 #   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
-ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, None)}
+#   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
+#   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop).
+ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000)}
+
+
+def launches_per_step(bench, gt, sorted_):
+    """Our kernels per step: sort_count, scan_local, scan_add, sort_scatter (A1-A2), then the lookup
+    kernel; the unionized / hash group kernel is preceded by idx_prep (A3)."""
+    if not sorted_:
+        return 1
+    return 4 + (2 if (bench == "xs" and gt in (1, 2)) else 1)
+
+
+def load_profile(cfg, sorted_):
+    """ncu numbers of the dominant kernel, committed under profiles/ (per-launch DRAM bytes)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{cfg}{'' if sorted_ else '_nosort'}")
 
 
 def env_int(k, d):
@@ -308,23 +327,33 @@ def main():
         alg_bytes, alg_flops = ALG[args.config]
         per_launch_lookups = n  # one lookup-kernel launch per step per rank
         look_avg_s = look_tot / K * 1e-3
-        roof = None
-        if bench == "xs":
-            flops = alg_flops * per_launch_lookups
-            roof = {"bound": "alu", "kernel": f"xs_lookup_{'sorted' if flags else 'direct'}<grid {gt}>",
-                    "achieved": flops / look_avg_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
-                    "unit": "TFLOP/s", "traffic": None,
-                    "note": f"{alg_flops} fp64 flops/lookup (SURVEY 8(d); division counted once) x {per_launch_lookups} "
-                            f"lookups per launch / mean launch time; peak = non-FMA fp64 op rate ({peaks['probe_src']})"}
-            roof["frac"] = roof["achieved"] / roof["peak"]
+        gname = {0: "nuclide", 1: "unionized", 2: "hash"}.get(gt, "")
+        if bench == "rs":
+            kname = "rs_lookup_sorted" if flags else "rs_lookup_direct"
+        elif not flags:
+            kname = f"xs_lookup_direct<{gname}>"
+        elif gt == 0:
+            kname = "xs_lookup_sorted<nuclide>"
+        else:
+            kname = f"xs_lookup_group<{gname}> (+ idx_prep, ~1% of the stage)"
+        flops = alg_flops * per_launch_lookups
+        prof = load_profile(args.config, not args.no_sort)
+        roof = {"bound": "alu", "kernel": kname,
+                "achieved": flops / look_avg_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
+                "unit": "TFLOP/s", "traffic": prof.get("dram_bytes") if prof else None,
+                "note": f"{alg_flops} fp64 flops/lookup (DESIGN.md Sec. 5; division counted once) x "
+                        f"{per_launch_lookups} lookups per launch / mean stage time (CUDA events on the launch "
+                        f"stream); peak = measured non-FMA FP64 op rate ({peaks['probe_src']}); traffic = ncu "
+                        f"dram read+write bytes per launch ({prof.get('src') if prof else 'no capture'})"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof_hbm = None
+        if alg_bytes:
             gb = alg_bytes * per_launch_lookups / look_avg_s / 1e9
             roof_hbm = {"bound": "hbm", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": gb / peaks["hbm_gbs"], "note": f"{alg_bytes} B/lookup random-order sector model "
                         f"(SURVEY 8(d)); >1 means the sort removed algorithmic bytes ({peaks['src']})"}
-        else:
-            roof = {"bound": "alu", "kernel": "rs_lookup_sorted", "achieved": None, "peak": None, "unit": None,
-                    "frac": None, "traffic": None}
-            roof_hbm = None
+            if prof and prof.get("dram_bytes"):
+                roof_hbm["dram_GBps_measured"] = prof["dram_bytes"] / look_avg_s / 1e9
         cb = None
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_baseline(args.config)
@@ -337,7 +366,7 @@ def main():
                        "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
                        "parallelism": f"lookup shards x{world}, grid replicated, 1 int64 NCCL all-reduce/step"},
             "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": K * (4 if flags else 1),
+            "gpu_launches": K * launches_per_step(bench, gt, flags),
             "clocks": clk,
             "stage_ms": {"sort": statistics.median(sort_ms), "lookup": statistics.median(look_ms),
                          "step": statistics.median(step_ms), "grid_build": grid_ms},

@@ -160,15 +160,27 @@ __device__ __noinline__ cplx faddeeva_abrarov(cplx Z) {
   return cadd(W, cmul({0.0, 8.124330e+01}, zs));
 }
 
+// W(Z).  The branch decision |Z| < 6 is computed exactly as the oracle does (RN products, RN sum,
+// correctly rounded sqrt), so both sides take the same branch.  The asymptotic branch (99.5% of
+// evaluations) is reassociated to one reciprocal instead of the four divisions of two complex
+// divisions:  a / P + c / Q = (a conj(P) |Q|^2 + c conj(Q) |P|^2) / (|P|^2 |Q|^2),  P = Z^2 - b,
+// Q = Z^2 - d  (|Z| >= 6 keeps |P|^2, |Q|^2 in [1e3, 2e8]: no overflow or cancellation); FMA is
+// allowed here (rs.cu is built -fmad=true) -- RSBench parity is 1e-10 x S (R-UNIQ).
 __device__ __forceinline__ cplx faddeeva(cplx Z) {
-  if (sqrt(Z.r * Z.r + Z.i * Z.i) < 6.0) return faddeeva_abrarov(Z);
+  const double az = sqrt(__dadd_rn(__dmul_rn(Z.r, Z.r), __dmul_rn(Z.i, Z.i)));
+  if (az < 6.0) return faddeeva_abrarov(Z);
   constexpr double a = 0.512424224754768462984202823134979415014943561548661637413182;
   constexpr double b = 0.275255128608410950901357962647054304017026259671664935783653;
   constexpr double c = 0.051765358792987823963876628425793170829107067780337219430904;
   constexpr double d = 2.724744871391589049098642037352945695982973740328335064216346;
-  cplx Z2 = cmul(Z, Z);
-  cplx t = cadd(cdiv({a, 0.0}, {Z2.r - b, Z2.i}), cdiv({c, 0.0}, {Z2.r - d, Z2.i}));
-  return cmul({-Z.i, Z.r}, t);  // (Z * i) * t
+  const double z2r = Z.r * Z.r - Z.i * Z.i, z2i = 2.0 * Z.r * Z.i;
+  const double pr = z2r - b, qr = z2r - d;  // imaginary parts of P and Q are z2i
+  const double i2 = z2i * z2i;
+  const double np = pr * pr + i2, nq = qr * qr + i2;
+  const double rinv = 1.0 / (np * nq);
+  const double ap = a * nq * rinv, cq = c * np * rinv;  // a / |P|^2, c / |Q|^2
+  const double sr = ap * pr + cq * qr, si = -(ap + cq) * z2i;
+  return {-Z.i * sr - Z.r * si, Z.r * sr - Z.i * si};  // (i Z) (sr + i si)
 }
 
 // ------------------------------------------------------------------------------------------ lookup
@@ -211,7 +223,10 @@ __device__ __forceinline__ void rs_macro(const RsDev &R, const Tables &T, double
       const int l = __ldg(R.pole_l + pbase + p);
       cplx Z = {(E - EA.x) * 0.5, (0.0 - EA.y) * 0.5};
       cplx fw = faddeeva(Z);
-      cplx wf = cmul(fw, fac[l]);
+      // fac[l] by selects (a dynamic index would put fac in local memory)
+      const double fr = l == 0 ? fac[0].r : (l == 1 ? fac[1].r : (l == 2 ? fac[2].r : fac[3].r));
+      const double fi = l == 0 ? fac[0].i : (l == 1 ? fac[1].i : (l == 2 ? fac[2].i : fac[3].i));
+      const cplx wf = {fw.r * fr - fw.i * fi, fw.r * fi + fw.i * fr};
       sT += RT.x * wf.r - RT.y * wf.i;
       sA += RA.x * fw.r - RA.y * fw.i;
       sF += RF.x * fw.r - RF.y * fw.i;

@@ -392,19 +392,18 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 // ------------------------------------------------------------------------------------------ production
 #include "xs_sorted_u.cuh"
 
-// Kernel for the sorted unionized path.  GF_XS_KERNEL in the environment selects an alternative for
-// A/B measurements: "staged" (TMA producer/consumer ring), "thread" (non-persistent, one lookup per
-// thread), "ring" (persistent, one lookup per thread, register-ring lookahead); default "group"
-// (persistent, kL lookups per thread).  All give identical results.
-enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2, kKernRing = 3 };
-static int sorted_u_kernel() {
+// Kernel for the sorted path.  GF_XS_KERNEL in the environment selects an alternative for A/B
+// measurements: "staged" (TMA producer/consumer ring, unionized only), "thread" (non-persistent,
+// one lookup per thread); default "group" (persistent, kL lookups per thread; unionized and hash
+// grids).  All give identical results.
+enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2 };
+static int sorted_kernel() {
   static int v = -1;
   if (v < 0) {
     const char *s = getenv("GF_XS_KERNEL");
     v = kKernGroup;
     if (s && s[0] == 's') v = kKernStaged;
     if (s && s[0] == 't') v = kKernThread;
-    if (s && s[0] == 'r') v = kKernRing;
   }
   return v;
 }
@@ -419,15 +418,12 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, macro_out != nullptr, st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernStaged)
+    if (GT == GF_GRID_UNIONIZED && sorted_kernel() == kKernStaged)
       return X.fastdiv ? launch_staged<true>(X, n, S, macro_out, vsum, st)
                        : launch_staged<false>(X, n, S, macro_out, vsum, st);
-    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernRing)
-      return X.fastdiv ? launch_sorted_u<true>(X, n, S, macro_out, vsum, st)
-                       : launch_sorted_u<false>(X, n, S, macro_out, vsum, st);
-    if (GT == GF_GRID_UNIONIZED && sorted_u_kernel() == kKernGroup)
-      return X.fastdiv ? launch_sorted_u4<true>(X, n, S, macro_out, vsum, st)
-                       : launch_sorted_u4<false>(X, n, S, macro_out, vsum, st);
+    if (GT != GF_GRID_NUCLIDE && sorted_kernel() != kKernThread)
+      return X.fastdiv ? launch_group<GT, true>(X, n, S, macro_out, vsum, st)
+                       : launch_group<GT, false>(X, n, S, macro_out, vsum, st);
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;

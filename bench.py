@@ -67,51 +67,56 @@ def env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event (throttle) reasons polled through NVML every ~2 ms during the timed
+    region (the timed region of a C3 step is a few ms, shorter than nvidia-smi's sampling period).
+    Same fields as B200_PROFILING.md's nvidia-smi clocks line."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop, self.t = index, [], threading.Event(), None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # no NVML: report unsampled
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                self.rows.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                  N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        if not sm:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        mx = max(float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit())
+        sm = [r[0] for r in self.rows]
         reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for nm, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
+        for _, bits in self.rows:
+            for nm, attr in self.REASONS.items():
+                if bits & getattr(self.N, attr, 0):
                     reasons.add(nm)
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.mx, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "NVML every 2 ms"}
 
 
 def load_peaks():
@@ -214,11 +219,17 @@ def main():
     from paper_2306_11686_b200 import build as gfbuild
     if rank == 0 and gfbuild.needs_build():
         gfbuild.build()
+    # one process per GPU; GF_DIST_BACKEND=gloo lets several ranks share one GPU (path tests only)
+    backend = os.environ.get("GF_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
     dev = torch.device("cuda", local)
     bench, n_iso, gt, n_total, desc = CONFIGS[args.config]
@@ -364,7 +375,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
             "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n,
                        "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
-                       "parallelism": f"lookup shards x{world}, grid replicated, 1 int64 NCCL all-reduce/step"},
+                       "parallelism": f"lookup shards x{world}, grid replicated, 1 int64 "
+                                      f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
             "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": K * launches_per_step(bench, gt, flags),
             "clocks": clk,

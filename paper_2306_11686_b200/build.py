@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         name = os.path.basename(src)
         obj = os.path.join(OBJ, name + ".o")
-        cmd = [nvcc(), *COMMON, *PER_FILE.get(name, DEFAULT), inc, "-c", src, "-o", obj]
+        extra = os.environ.get("GF_EXTRA_NVCC", "").split()  # tuning A/B only (e.g. -DGF_GROUP_L=2)
+        cmd = [nvcc(), *COMMON, *PER_FILE.get(name, DEFAULT), *extra, inc, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {name}:\n" + res.stderr[-8000:])

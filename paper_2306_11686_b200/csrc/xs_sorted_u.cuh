@@ -19,7 +19,13 @@
 // or register-file overflow).
 #pragma once
 
-constexpr int kL = 4;
+#ifndef GF_GROUP_L
+#define GF_GROUP_L 4
+#endif
+#ifndef GF_GROUP_MINB
+#define GF_GROUP_MINB 3
+#endif
+constexpr int kL = GF_GROUP_L;  // lookups per thread (A/B: -DGF_GROUP_L=2 -DGF_GROUP_MINB=5)
 constexpr int kTpbL = 128;
 constexpr int kIgPf = 10;  // index-/hash-grid L2 prefetch distance (nuclides)
 
@@ -97,7 +103,7 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
 }
 
 template <int GT, bool FAST>
-__global__ void __launch_bounds__(kTpbL, 3)
+__global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
     xs_lookup_group(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
                     const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart,
                     double *__restrict__ macro_out, unsigned long long *__restrict__ vsum) {

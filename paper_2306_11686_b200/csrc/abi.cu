@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -195,6 +196,17 @@ struct gf_xs_grid {
   XsDev xs{};
   RsDev rs{};
   ArrView arr[32];
+  // host-IO pipeline objects (created on first GF_HOST_IO call; calls serialise on io_mu)
+  std::mutex io_mu;
+  bool io_ready = false;
+  cudaStream_t io_s[3] = {};
+  cudaEvent_t io_ev[7] = {};
+  ~gf_xs_grid() {
+    if (!io_ready) return;
+    DeviceGuard dg(device);
+    for (auto s : io_s) cudaStreamDestroy(s);
+    for (auto e : io_ev) cudaEventDestroy(e);
+  }
 };
 
 extern "C" {
@@ -384,13 +396,27 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 }
 
 // ------------------------------------------------------------------------------------------ lookups
+// Scratch of one lookup slot.  Device-resident calls use one slot sized for the whole batch.  Host-IO
+// calls (GF_HOST_IO) are pipelined in chunks of kIoChunk lookups over two slots and three streams:
+// chunk c's host->device copy, chunk c-1's lookup and chunk c-2's device->host copy overlap (PCIe is
+// full duplex).  Each chunk is sorted and looked up on its own; results are identical.
+constexpr uint64_t kIoChunk = 1ull << 21;
+
+struct SlotLayout {
+  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, h_macro, h_E, h_mat, bytes;
+};
 struct BatchLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, h_macro, h_vsum, h_E, h_mat, total;
+  SlotLayout slot;
+  int slots;
+  size_t h_vsum, total;
 };
 
 static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
                        BatchLayout &B) {
   memset(&B, 0, sizeof B);
+  const bool host_io = (flags & GF_HOST_IO) != 0;
+  const uint64_t m = host_io ? (n < kIoChunk ? n : kIoChunk) : n;
+  SlotLayout &L = B.slot;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -399,24 +425,26 @@ static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool wan
   };
   const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
   if (flags & GF_SORT_LOCALITY) {
-    B.counts = take(sizeof(uint32_t) * kBins);
-    B.cursor = take(sizeof(uint32_t) * kBins);
-    B.btot = take(sizeof(uint32_t) * (kBins / kScanBlk));
-    B.mstart = take(sizeof(uint32_t) * 16);
-    B.Es = take(sizeof(double) * n);
-    B.idx = take(sizeof(uint32_t) * n);
-    B.us = take(sizeof(uint32_t) * n);
-    B.tinfo = take(32 * ((n + 127) / 128));
+    L.counts = take(sizeof(uint32_t) * kBins);
+    L.cursor = take(sizeof(uint32_t) * kBins);
+    L.btot = take(sizeof(uint32_t) * (kBins / kScanBlk));
+    L.mstart = take(sizeof(uint32_t) * 16);
+    L.Es = take(sizeof(double) * m);
+    L.idx = take(sizeof(uint32_t) * m);
+    L.us = take(sizeof(uint32_t) * m);
+    L.tinfo = take(32 * ((m + 127) / 128));
   }
-  if (flags & GF_HOST_IO) {
-    if (want_macro) B.h_macro = take(sizeof(double) * ch * n);
-    B.h_vsum = take(sizeof(uint64_t));
+  if (host_io) {
+    if (want_macro) L.h_macro = take(sizeof(double) * ch * m);
     if (energies) {
-      B.h_E = take(sizeof(double) * n);
-      B.h_mat = take(n);
+      L.h_E = take(sizeof(double) * m);
+      L.h_mat = take(m);
     }
   }
-  B.total = o > 0 ? o : 256;
+  L.bytes = al(o > 0 ? o : 256);
+  B.slots = host_io ? 2 : 1;
+  B.h_vsum = B.slots * L.bytes;
+  B.total = B.h_vsum + (host_io ? 256 : 0);
 }
 
 gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes) {
@@ -424,6 +452,87 @@ gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t fl
   BatchLayout B;
   plan_batch(g, n_lookups, flags, true, true, B);  // upper bound over the optional parts
   *scratch_bytes = B.total;
+  return GF_OK;
+}
+
+static SortScratch slot_sort(char *base, const SlotLayout &L) {
+  SortScratch S{};
+  S.counts = reinterpret_cast<uint32_t *>(base + L.counts);
+  S.cursor = reinterpret_cast<uint32_t *>(base + L.cursor);
+  S.btot = reinterpret_cast<uint32_t *>(base + L.btot);
+  S.mstart = reinterpret_cast<uint32_t *>(base + L.mstart);
+  S.Es = reinterpret_cast<double *>(base + L.Es);
+  S.idx = reinterpret_cast<uint32_t *>(base + L.idx);
+  S.us = reinterpret_cast<uint32_t *>(base + L.us);
+  S.tinfo = base + L.tinfo;
+  return S;
+}
+
+static cudaError_t launch_lookup(const gf_xs_grid *g, uint64_t first, uint32_t n, uint64_t seed, const double *dE,
+                                 const uint8_t *dmat, bool sort, const SortScratch &S, double *dmacro,
+                                 unsigned long long *dvsum, cudaStream_t st, cudaEvent_t ev_mid) {
+  return g->p.bench == GF_XSBENCH
+             ? launch_xs_lookup(g->xs, first, n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid)
+             : launch_rs_lookup(g->rs, first, n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid);
+}
+
+// Internal streams / events of the host-IO pipeline (created on first use, per grid).
+static gf_status io_setup(gf_xs_grid *g) {
+  if (g->io_ready) return GF_OK;
+  for (int i = 0; i < 3; i++) GF_CUDA(cudaStreamCreateWithFlags(&g->io_s[i], cudaStreamNonBlocking));
+  for (int i = 0; i < 7; i++) GF_CUDA(cudaEventCreateWithFlags(&g->io_ev[i], cudaEventDisableTiming));
+  g->io_ready = true;
+  return GF_OK;
+}
+
+static gf_status run_host_io(const gf_xs_grid *gc, uint64_t first, uint64_t n, uint64_t seed, const double *E,
+                             const uint8_t *mat, bool sort, double *macro_out, uint64_t *vsum, char *sc,
+                             const BatchLayout &B, cudaStream_t st) {
+  gf_xs_grid *g = const_cast<gf_xs_grid *>(gc);  // the pipeline objects are the only mutable state
+  std::lock_guard<std::mutex> lock(g->io_mu);
+  gf_status s = io_setup(g);
+  if (s != GF_OK) return s;
+  cudaStream_t sin = g->io_s[0], scomp = g->io_s[1], sout = g->io_s[2];
+  cudaEvent_t start = g->io_ev[0], *h2d = g->io_ev + 1, *comp = g->io_ev + 3, *d2h = g->io_ev + 5;
+  const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
+  const bool energies = E != nullptr;
+  unsigned long long *dvsum = reinterpret_cast<unsigned long long *>(sc + B.h_vsum);
+  GF_CUDA(cudaEventRecord(start, st));  // ordered after the caller's prior work on `stream`
+  GF_CUDA(cudaStreamWaitEvent(sin, start, 0));
+  GF_CUDA(cudaStreamWaitEvent(scomp, start, 0));
+  GF_CUDA(cudaMemsetAsync(dvsum, 0, 8, scomp));
+  const uint64_t nch = (n + kIoChunk - 1) / kIoChunk;
+  for (uint64_t c = 0; c < nch; c++) {
+    const int k = (int)(c & 1);
+    const uint64_t off = c * kIoChunk, cn = (n - off < kIoChunk) ? n - off : kIoChunk;
+    char *base = sc + k * B.slot.bytes;
+    const SlotLayout &L = B.slot;
+    if (c >= 2) GF_CUDA(cudaStreamWaitEvent(sin, d2h[k], 0));  // slot k free (chunk c-2 copied out)
+    const double *dE = nullptr;
+    const uint8_t *dmat = nullptr;
+    if (energies) {
+      GF_CUDA(cudaMemcpyAsync(base + L.h_E, E + off, sizeof(double) * cn, cudaMemcpyHostToDevice, sin));
+      GF_CUDA(cudaMemcpyAsync(base + L.h_mat, mat + off, cn, cudaMemcpyHostToDevice, sin));
+      dE = reinterpret_cast<const double *>(base + L.h_E);
+      dmat = reinterpret_cast<const uint8_t *>(base + L.h_mat);
+    }
+    GF_CUDA(cudaEventRecord(h2d[k], sin));
+    GF_CUDA(cudaStreamWaitEvent(scomp, h2d[k], 0));
+    double *dmacro = macro_out ? reinterpret_cast<double *>(base + L.h_macro) : nullptr;
+    cudaError_t ce = launch_lookup(g, first + off, (uint32_t)cn, seed, dE, dmat, sort, slot_sort(base, L), dmacro,
+                                   dvsum, scomp, nullptr);
+    if (ce != cudaSuccess) return fail(GF_E_CUDA, "lookup launch: %s", cudaGetErrorString(ce));
+    GF_CUDA(cudaEventRecord(comp[k], scomp));
+    GF_CUDA(cudaStreamWaitEvent(sout, comp[k], 0));
+    if (macro_out)
+      GF_CUDA(cudaMemcpyAsync(macro_out + off * ch, dmacro, sizeof(double) * ch * cn, cudaMemcpyDeviceToHost, sout));
+    GF_CUDA(cudaEventRecord(d2h[k], sout));
+  }
+  uint64_t add = 0;
+  GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, scomp));
+  GF_CUDA(cudaStreamSynchronize(scomp));
+  GF_CUDA(cudaStreamSynchronize(sout));
+  *vsum += add;
   return GF_OK;
 }
 
@@ -448,50 +557,16 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
   if (!dg.ok) return fail(GF_E_CUDA, "cannot make device %d current", g->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   char *sc = static_cast<char *>(scratch);
-  const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
-
-  const double *dE = E;
-  const uint8_t *dmat = mat;
-  double *dmacro = macro_out;
-  unsigned long long *dvsum = reinterpret_cast<unsigned long long *>(vsum);
-  if (host_io) {
-    dvsum = reinterpret_cast<unsigned long long *>(sc + B.h_vsum);
-    GF_CUDA(cudaMemsetAsync(dvsum, 0, 8, st));
-    if (macro_out) dmacro = reinterpret_cast<double *>(sc + B.h_macro);
-    if (energies) {
-      GF_CUDA(cudaMemcpyAsync(sc + B.h_E, E, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-      GF_CUDA(cudaMemcpyAsync(sc + B.h_mat, mat, n, cudaMemcpyHostToDevice, st));
-      dE = reinterpret_cast<const double *>(sc + B.h_E);
-      dmat = reinterpret_cast<const uint8_t *>(sc + B.h_mat);
-    }
-  }
-  SortScratch S{};
   const bool sort = (flags & GF_SORT_LOCALITY) != 0;
-  if (sort) {
-    S.counts = reinterpret_cast<uint32_t *>(sc + B.counts);
-    S.cursor = reinterpret_cast<uint32_t *>(sc + B.cursor);
-    S.btot = reinterpret_cast<uint32_t *>(sc + B.btot);
-    S.mstart = reinterpret_cast<uint32_t *>(sc + B.mstart);
-    S.Es = reinterpret_cast<double *>(sc + B.Es);
-    S.idx = reinterpret_cast<uint32_t *>(sc + B.idx);
-    S.us = reinterpret_cast<uint32_t *>(sc + B.us);
-    S.tinfo = sc + B.tinfo;
-  }
+  if (host_io) return run_host_io(g, first, n, seed, E, mat, sort, macro_out, vsum, sc, B, st);
+
+  unsigned long long *dvsum = reinterpret_cast<unsigned long long *>(vsum);
   cudaEvent_t ev_mid = ev ? static_cast<cudaEvent_t>(ev->before_lookup) : nullptr;
   if (ev && ev->before_sort) GF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev->before_sort), st));
-  cudaError_t ce = g->p.bench == GF_XSBENCH
-                       ? launch_xs_lookup(g->xs, first, (uint32_t)n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid)
-                       : launch_rs_lookup(g->rs, first, (uint32_t)n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid);
+  cudaError_t ce = launch_lookup(g, first, (uint32_t)n, seed, E, mat, sort, slot_sort(sc, B.slot), macro_out, dvsum,
+                                 st, ev_mid);
   if (ce != cudaSuccess) return fail(GF_E_CUDA, "lookup launch: %s", cudaGetErrorString(ce));
   if (ev && ev->after_lookup) GF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev->after_lookup), st));
-  if (host_io) {
-    uint64_t add = 0;
-    if (macro_out)
-      GF_CUDA(cudaMemcpyAsync(macro_out, dmacro, sizeof(double) * ch * n, cudaMemcpyDeviceToHost, st));
-    GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, st));
-    GF_CUDA(cudaStreamSynchronize(st));
-    *vsum += add;
-  }
   return GF_OK;
 }
 

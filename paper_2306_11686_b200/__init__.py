@@ -234,9 +234,10 @@ class Grid:
         raw = int(vsum.item())
         return (raw, macro) if want_macro else raw
 
-    def lookup_energies(self, E, mat, sort: bool = True, want_macro: bool = True, stream=None):
+    def lookup_energies(self, E, mat, sort: bool = True, want_macro: bool = True, stream=None, out=None):
         """Caller-supplied states.  Device tensors -> device outputs; pinned/CPU tensors -> the call
-        stages them (GF_HOST_IO) and returns host outputs."""
+        stages them (GF_HOST_IO, pipelined H2D / lookup / D2H) and returns host outputs.  `out`: an
+        optional preallocated [n][5|4] fp64 output (pinned for host I/O) reused across calls."""
         torch = self.torch
         n = E.numel()
         host = not E.is_cuda
@@ -245,7 +246,9 @@ class Grid:
         st = _stream_ptr(torch, stream)
         if host:
             vs = C.c_uint64(0)
-            macro = torch.empty((n, self.channels), dtype=torch.float64, pin_memory=True) if want_macro else None
+            macro = out
+            if want_macro and macro is None:
+                macro = torch.empty((n, self.channels), dtype=torch.float64, pin_memory=True)
             _check(lib().gf_xs_lookup_energies(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()), n, flags,
                                                C.c_void_p(macro.data_ptr()) if want_macro else None, C.byref(vs),
                                                C.c_void_p(sc.data_ptr()), sc.numel(), st))

@@ -304,7 +304,7 @@ def main():
 
     # ---------------------------------------------------------------- end-to-end through the public API
     e2e = None
-    if not args.no_e2e and bench == "xs":
+    if not args.no_e2e:
         import numpy as np
         rng = np.random.default_rng(1234 + rank)
         P = np.array([0.139, 0.052, 0.275, 0.134, 0.154, 0.064, 0.066, 0.055, 0.008, 0.015, 0.025, 0.013])
@@ -329,9 +329,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = t.item()
         e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 9 * n,
-               "d2h_bytes_per_step": (40 * n + 8),
-               "path": "gf_xs_lookup_energies with GF_HOST_IO: pinned host E[n] (f64) + mat[n] (u8) in, "
-                       "macro[n][5] (f64) + raw out, per rank; host-timed incl. copies and sync"}
+               "d2h_bytes_per_step": (8 * grid.channels * n + 8),
+               "path": f"gf_xs_lookup_energies with GF_HOST_IO: pinned host E[n] (f64) + mat[n] (u8) in, "
+                       f"macro[n][{grid.channels}] (f64) + raw out, per rank; host-timed incl. copies and sync"}
         del Eh, mh
 
     if rank == 0:

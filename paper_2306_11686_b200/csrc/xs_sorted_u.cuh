@@ -51,10 +51,34 @@ __device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_ba
   }
 }
 
+#ifndef GF_SHORTCUT
+#define GF_SHORTCUT 1
+#endif
+
 // Interval indices of the kL lookups for the nuclide of table entry e.
+// Unionized grid: one u16 index-grid load per lookup.
+// Hash grid: interval shortcut (DESIGN.md R-SHORT).  Lookup 0's interval k0 is searched literally;
+// a lookup i in the same hash bin with A[k0] < E_i < A[k0+1] has interval k0 as well -- the bin's
+// edge rules cannot fire for it and the bisection returns the unique k with A[k] <= E_i < A[k+1] --
+// so only the rare others are searched.  Grid energies are LCG doubles in [+0, 1): the test compares
+// bit patterns as signed 64-bit integers, which order exactly like the doubles for every E_i (NaN,
+// -0 and negatives fail it and take the literal search).  (Measured: splitting
+// the hash search into two pipeline stages, with or without L1 prefetch of the energies, is slower.)
 template <int GT>
 __device__ __forceinline__ void load_k(const XsDev &X, uint2 e, const double (&E)[kL], const uint32_t (&ix)[kL],
                                        uint32_t (&k)[kL]) {
+  if (GT == GF_GRID_HASH && GF_SHORTCUT) {
+    const uint32_t k0 = interval<GT>(X, e, E[0], ix[0]);
+    const long long lo = __double_as_longlong(__ldg(X.Ed + e.x + k0));
+    const long long hi = __double_as_longlong(__ldg(X.Ed + e.x + k0 + 1));
+    k[0] = k0;
+#pragma unroll
+    for (int i = 1; i < kL; i++) {
+      const long long v = __double_as_longlong(E[i]);
+      k[i] = (ix[i] == ix[0] && lo < v && v < hi) ? k0 : interval<GT>(X, e, E[i], ix[i]);
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kL; i++) {
     if (GT == GF_GRID_UNIONIZED)

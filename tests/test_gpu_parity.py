@@ -316,6 +316,34 @@ def test_energies_api_device_and_host(gf, torch, grid_type):
     assert raw_h == raw_o and np.array_equal(m_h.numpy(), m_o)
 
 
+@pytest.mark.parametrize("grid_type", [1, 2])
+def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
+    """Sorted lookups share record pairs and (hash grid) the interval shortcut R-SHORT, which takes
+    lookup 0's interval for a group-mate strictly inside it.  Clusters of one material around exact
+    gridpoints, hash-bin edges and repeated energies put ties, 1-ulp neighbours and interval
+    crossings inside the same groups of 4; every macro xs must still equal the oracle's bitwise."""
+    o, g = make_pair(gf, 68, 11303, grid_type)
+    rng = np.random.default_rng(77)
+    G = o.nuclide_grid()
+    Es = []
+    for nuc in (0, 2, 5, 41, 60, 67):
+        for k in list(rng.integers(0, o.n_gp - 1, 6)) + [0, o.n_gp - 2, o.n_gp - 1]:
+            e = float(G[nuc, k, 0])
+            Es += [e, e, math.nextafter(e, 0), math.nextafter(e, 2), e, math.nextafter(e, 2)]
+            Es += list(e + (rng.random(10) - 0.5) * 2e-4)
+    for b in list(rng.integers(1, 10000, 20)) + [1, 9999]:
+        e = b * (1.0 / 10000)
+        Es += [e, math.nextafter(e, 0), math.nextafter(e, 2), e, math.nextafter(math.nextafter(e, 0), 0)]
+    Es += list(0.3 + rng.random(20000) * 1e-3)  # dense: about 20 lookups per interval per nuclide
+    E = np.clip(np.array(Es), 0.0, 1.0)
+    for mat in (0, 4, 7):
+        mats = np.full(len(E), mat, dtype=np.uint8)
+        raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
+        raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
+        assert raw_g == raw_o
+        assert np.array_equal(m_g.cpu().numpy(), m_o), f"mat {mat}"
+
+
 def test_host_io_pipeline_chunks(gf, torch):
     """GF_HOST_IO pipelines chunks of 2^21 lookups over two slots and three streams; with several
     chunks and a ragged last one the outputs equal the device-resident call's, and the oracle's."""

@@ -100,7 +100,7 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   // XS
-  size_t G, Ed, Rd, flags, U, IG, HG, ubin;
+  size_t G, Ed, Rd, XR, flags, U, IG, HG, ubin;
   long long ig_pitch;
   int hg_pitch;
   // RS
@@ -150,6 +150,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.Ed = take(npts * 8);
     L.Rd = take(npts * 8 + 16);  // +16: the staged kernel's bulk copies round ranges up to 16 B
     L.flags = take(16);
+    if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128);
     if (p->grid_type == GF_GRID_UNIONIZED) {
       L.ig_pitch = (long long)((npts + 63) & ~size_t(63));
       L.U = take(npts * 8);
@@ -326,11 +327,12 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       double *Ed = reinterpret_cast<double *>(base + L.Ed);
       double *Rd = reinterpret_cast<double *>(base + L.Rd);
       int *zero_width = reinterpret_cast<int *>(base + L.flags);
+      double *XR = X.grid_type != GF_GRID_NUCLIDE ? reinterpret_cast<double *>(base + L.XR) : nullptr;
       double *U = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<double *>(base + L.U) : nullptr;
       uint16_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint16_t *>(base + L.IG) : nullptr;
       uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
       uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
-      X.G = G; X.Ed = Ed; X.Rd = Rd; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
+      X.G = G; X.Ed = Ed; X.Rd = Rd; X.XR = XR; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
       const size_t npts = (size_t)X.n_union;
       put(GF_ARR_NUCLIDE_GRID, G, npts * 48, X.n_gp);
@@ -340,7 +342,8 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 2, X.hg_pitch);
       if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
       put(GF_ARR_RECIP_WIDTH, Rd, npts * 8, X.n_gp);
-      ce = launch_xs_grid(X, G, Ed, Rd, zero_width, U, IG, HG, ubin, mconc, p->init_seed,
+      if (XR) put(GF_ARR_INTERVALS, XR, npts * 128, X.n_gp);
+      ce = launch_xs_grid(X, G, Ed, Rd, XR, zero_width, U, IG, HG, ubin, mconc, p->init_seed,
                           static_cast<double *>(scratch), st);
       // the exact reciprocal division is used only if no interval has zero (or underflowing) width
       int zw = 1;

@@ -103,6 +103,28 @@ __global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, dou
   }
 }
 
+// ------------------------------------------------------------------------------------------ K0b'
+// Interval records for the sorted lookup kernel, one 128-B line per interval k < n_gp - 1 of each
+// nuclide (layout in gf_internal.cuh XsDev::XR).  Every stored difference / reciprocal is the RN
+// operation the lookup would otherwise do per micro evaluation (R-FP), so results are unchanged.
+__global__ void __launch_bounds__(256) xr_build(const double *__restrict__ G, const double *__restrict__ Rd,
+                                                double *__restrict__ XR, long long npts, int n_gp) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= npts) return;
+  double2 *o = reinterpret_cast<double2 *>(XR + r * 16);
+  if ((int)(r % n_gp) == n_gp - 1) {  // no interval starts at the last gridpoint
+#pragma unroll
+    for (int q = 0; q < 8; q++) o[q] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double *lo = G + r * 6, *hi = lo + 6;
+  o[0] = make_double2(hi[0], __dsub_rn(hi[0], lo[0]));
+#pragma unroll
+  for (int c = 0; c < 5; c++) o[1 + c] = make_double2(hi[1 + c], __dsub_rn(hi[1 + c], lo[1 + c]));
+  o[6] = make_double2(Rd[r], lo[0]);
+  o[7] = make_double2(0.0, 0.0);
+}
+
 // ------------------------------------------------------------------------------------------ K0c
 // One merge round: runs of length L (last may be shorter) are merged pairwise.  An element of a
 // left run goes before partner elements equal to it (lower bound), an element of a right run after
@@ -214,9 +236,9 @@ __global__ void concs_fill(double *__restrict__ conc, int total, uint64_t seed, 
 
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, int *zero_width, double *U,
-                           uint16_t *IG, uint16_t *HG, uint32_t *ubin, double *mconc, uint64_t seed, double *scratch,
-                           cudaStream_t st) {
+cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, double *XR, int *zero_width,
+                           double *U, uint16_t *IG, uint16_t *HG, uint32_t *ubin, double *mconc, uint64_t seed,
+                           double *scratch, cudaStream_t st) {
   cudaError_t e;
   const long long npts = (long long)X.n_iso * X.n_gp;
   int npow = 2;
@@ -228,6 +250,10 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, in
   if ((e = cudaMemsetAsync(zero_width, 0, sizeof(int), st)) != cudaSuccess) return e;
   xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, Rd, zero_width, X.n_gp, npow, seed);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (XR) {
+    xr_build<<<nblk(npts, 256), 256, 0, st>>>(G, Rd, XR, npts, X.n_gp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
 
   concs_fill<<<nblk(X.total, 256), 256, 0, st>>>(mconc, X.total, seed, 6ull * (uint64_t)npts);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

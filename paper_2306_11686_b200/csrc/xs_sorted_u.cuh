@@ -38,16 +38,50 @@ __global__ void __launch_bounds__(256) idx_prep(XsDev X, uint32_t n, const doubl
   if (p < n) ix[p] = (uint32_t)energy_index<GT>(X, Es[p]);
 }
 
+// One interval record of XsDev::XR: v0 = (E[k+1], E[k+1] - E[k]), v(1+c) = (xs_c[k+1],
+// xs_c[k+1] - xs_c[k]), y = RN(1 / (E[k+1] - E[k])).  Six 16-B loads and one 8-B load from one
+// 128-B line (4 sectors), the same instruction count as the 96-B record pair of G plus Rd.
+struct Rec {
+  double2 v0, v1, v2, v3, v4, v5;
+  double y;  // fast division path only
+};
+
 template <bool FAST>
-__device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_base, const uint32_t (&k)[kL], Pair &P,
+__device__ __forceinline__ void load_rec(const XsDev &X, uint32_t r, Rec &R) {
+  const double2 *p = reinterpret_cast<const double2 *>(X.XR) + (size_t)r * 8;
+  R.v0 = __ldg(p + 0);
+  R.v1 = __ldg(p + 1);
+  R.v2 = __ldg(p + 2);
+  R.v3 = __ldg(p + 3);
+  R.v4 = __ldg(p + 4);
+  R.v5 = __ldg(p + 5);
+  if (FAST) R.y = __ldg(X.XR + (size_t)r * 16 + 12);
+}
+
+// f = (hi.E - E) / (hi.E - lo.E); x_c = hi_c - f (hi_c - lo_c); m_c += x_c * conc -- the same RN
+// operations as accumulate() with the two grid-only differences read from the record.
+template <bool FAST>
+__device__ __forceinline__ void accumulate_rec(const Rec &R, double E, double conc, double m[5]) {
+  const double a = __dsub_rn(R.v0.x, E), b = R.v0.y;
+  const double f = FAST ? div_rn(a, b, R.y) : __ddiv_rn(a, b);
+  const double2 hd[5] = {R.v1, R.v2, R.v3, R.v4, R.v5};
+#pragma unroll
+  for (int c = 0; c < 5; c++) {
+    const double x = __dsub_rn(hd[c].x, __dmul_rn(f, hd[c].y));
+    m[c] = __dadd_rn(m[c], __dmul_rn(x, conc));
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_base, const uint32_t (&k)[kL], Rec &P,
                                                  uint32_t &kP, const double (&E)[kL], double conc, double (&m)[kL][5]) {
 #pragma unroll
   for (int i = 0; i < kL; i++) {
     if (k[i] != kP) {  // another interval than the staged pair (rare): reload
-      load_pair<FAST>(X, rec_base + k[i], P);
+      load_rec<FAST>(X, rec_base + k[i], P);
       kP = k[i];
     }
-    accumulate<FAST>(P, E[i], conc, m[i]);
+    accumulate_rec<FAST>(P, E[i], conc, m[i]);
   }
 }
 
@@ -102,21 +136,21 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
 #pragma unroll
   for (int i = 0; i < 3; i++)
     if (j0 + i < j1) load_k<GT>(X, T.ent[j0 + i], E, ix, kq[i]);
-  Pair A, B;
+  Rec A, B;
   uint32_t kA = kq[0][0], kB = 0xFFFFFFFFu;
-  load_pair<FAST>(X, T.ent[j0].x + kA, A);
+  load_rec<FAST>(X, T.ent[j0].x + kA, A);
   for (int j = j0; j < j1; j += 4) {
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const int jj = j + i;
       if (jj >= j1) break;
-      Pair &cur = (i & 1) ? B : A;
-      Pair &nxt = (i & 1) ? A : B;
+      Rec &cur = (i & 1) ? B : A;
+      Rec &nxt = (i & 1) ? A : B;
       uint32_t &kcur = (i & 1) ? kB : kA;
       uint32_t &knxt = (i & 1) ? kA : kB;
       if (jj + 1 < j1) {
         knxt = kq[(i + 1) & 3][0];
-        load_pair<FAST>(X, T.ent[jj + 1].x + knxt, nxt);
+        load_rec<FAST>(X, T.ent[jj + 1].x + knxt, nxt);
       }
       if (jj + kIgPf < j1)  // index-/hash-grid line of nuclide jj + kIgPf into L2 (no register cost)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(grid_line<GT>(X, T.ent[jj + kIgPf], ix[0])));
@@ -173,14 +207,14 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
         double mi[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         const bool fi = FAST && fabs(E[i]) <= 2.0;
         for (int j = j0; j < j1; j++) {  // plain loop: these lookups are a handful per batch
-          Pair P;
+          Rec P;
           const uint32_t rec = T.ent[j].x + interval<GT>(X, T.ent[j], E[i], ix[i]);
           if (fi) {
-            load_pair<FAST>(X, rec, P);
-            accumulate<FAST>(P, E[i], T.conc[j], mi);
+            load_rec<FAST>(X, rec, P);
+            accumulate_rec<FAST>(P, E[i], T.conc[j], mi);
           } else {
-            load_pair<false>(X, rec, P);
-            accumulate<false>(P, E[i], T.conc[j], mi);
+            load_rec<false>(X, rec, P);
+            accumulate_rec<false>(P, E[i], T.conc[j], mi);
           }
         }
 #pragma unroll

@@ -73,6 +73,18 @@ def check_arrays(o, g, full_ig=True):
     assert g.fastdiv == bool(np.all(w >= 2.0 ** -960))
     Ed = g.array("energy")[0].cpu().numpy().reshape(n_iso, n_gp)
     assert np.array_equal(Ed, o.nuclide_grid()[:, :, 0])
+    if o.grid_type != O.NUCLIDE:  # interval records: every stored value is one RN numpy operation
+        XR = g.array("intervals")[0].cpu().numpy().reshape(n_iso, n_gp, 16)
+        lo, hi = G[:, :-1, :], G[:, 1:, :]
+        with np.errstate(divide="ignore"):
+            want = np.zeros((n_iso, n_gp, 16))
+            want[:, :-1, 0] = hi[..., 0]
+            want[:, :-1, 1] = hi[..., 0] - lo[..., 0]
+            want[:, :-1, 2:12:2] = hi[..., 1:]
+            want[:, :-1, 3:12:2] = hi[..., 1:] - lo[..., 1:]
+            want[:, :-1, 12] = 1.0 / (hi[..., 0] - lo[..., 0])
+            want[:, :-1, 13] = lo[..., 0]
+        assert np.array_equal(XR, want)
     nn, mats, concs = o.tables()
     off = g.array("mat_offsets")[0].cpu().numpy()
     gc = g.array("concs")[0].cpu().numpy()

@@ -10,9 +10,9 @@
 //
 // The nuclide loop is software-pipelined at three distances: the interval indices of the kL lookups
 // 3 nuclides ahead (register ring, unrolled by 4 so it is statically indexed), the index- / hash-grid
-// line kIgPf nuclides ahead (prefetch.global.L2, no register cost), and the record pair of the next
-// nuclide (two buffers).  CTAs are persistent (grid = SMs x resident CTAs) and stage the material
-// tables in SMEM once.  A3 runs in a separate massively parallel pass (idx_prep) so its dependent
+// line kIgPf nuclides ahead (prefetch.global.L2, no register cost), the interval record 2 ahead
+// (prefetch.global.L1) and the record of the next nuclide (two register buffers).  CTAs are
+// persistent (grid = SMs x resident CTAs) and stage the material tables in SMEM once.  A3 runs in a separate massively parallel pass (idx_prep) so its dependent
 // search latency is not on this kernel's critical path.
 // Measured alternatives: one lookup per thread; a TMA/mbarrier producer-consumer
 // ring (xs_staged.cuh, selectable with GF_XS_KERNEL=staged); deeper register rings (instruction-cache
@@ -154,6 +154,8 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
       }
       if (jj + kIgPf < j1)  // index-/hash-grid line of nuclide jj + kIgPf into L2 (no register cost)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(grid_line<GT>(X, T.ent[jj + kIgPf], ix[0])));
+      if (jj + 2 < j1)  // the record of nuclide jj + 2 (its interval is in the ring) into L1
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(X.XR + (size_t)(T.ent[jj + 2].x + kq[(i + 2) & 3][0]) * 16));
       if (jj + 3 < j1) load_k<GT>(X, T.ent[jj + 3], E, ix, kq[(i + 3) & 3]);
       accumulate_group<FAST>(X, T.ent[jj].x, kq[i], cur, kcur, E, T.conc[jj], m);
     }

@@ -101,7 +101,7 @@ gf_status gf_xs_grid_free(gf_xs_grid *g);
  *   GF_ARR_UNIONIZED     double [n_iso*n_gp]      (unionized grid only)
  *   GF_ARR_INDEX_GRID    uint16 [n_iso][pitch]    nuclide-major IG, pitch = *pitch_out >= n_iso*n_gp
  *   GF_ARR_HASH_GRID     uint16 [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
- *   GF_ARR_UNION_BINS    uint32 [16385]           #{U < b / 2^14}: top level of the unionized search
+ *   GF_ARR_UNION_BINS    uint32 [2^20 + 1]        #{U < b / 2^20}: top level of the unionized search
  *   GF_ARR_RECIP_WIDTH   double [n_iso][n_gp]     RN(1 / (E[k+1] - E[k])) per interval (exact division)
  *   GF_ARR_INTERVALS     double [n_iso][n_gp][16] unionized / hash grids: per interval k < n_gp-1 the
  *                        sorted kernel's 128-B record E[k+1], E[k+1]-E[k], (xs_c[k+1], xs_c[k+1]-xs_c[k])

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, c
   for (int k = 0; k < 4; k++) dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
 }
 
-// Top-level table of the two-level unionized search: ubin[b] = #{U < b / 2^14}, ubin[2^14] = n.
+// Top-level table of the two-level unionized search: ubin[b] = #{U < b / 2^20}, ubin[2^20] = n.
 __global__ void ubin_build(const double *__restrict__ U, uint32_t *__restrict__ ubin, long long n_union) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > kUBins) return;
@@ -202,7 +202,7 @@ __global__ void ubin_build(const double *__restrict__ U, uint32_t *__restrict__ 
     ubin[b] = (uint32_t)n_union;
     return;
   }
-  const double edge = __dmul_rn((double)b, 0x1p-14);  // exact
+  const double edge = __dmul_rn((double)b, 1.0 / kUBins);  // exact
   long long lo = 0, hi = n_union;
   while (lo < hi) {
     long long mid = (lo + hi) >> 1;

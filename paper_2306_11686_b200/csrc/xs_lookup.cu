@@ -5,7 +5,7 @@
 //   A2  locality sort   counting sort by (material, energy bin): count -> two-kernel scan -> scatter
 //                       of E (and the original position when per-lookup outputs are requested).
 //                       Results are order-independent (integer hash; outputs go back by position).
-//   A3  energy search   unionized: two-level search of U (the 2^14-bin table ubin narrows the
+//   A3  energy search   unionized: two-level search of U (the 2^20-bin table ubin narrows the
 //                       bisection to one energy bin; same result as XSBench's grid_search, which is
 //                       clamp(#{U <= E} - 1, 0, n-2)); hash: (int64)(E / (1.0/bins)); nuclide: per
 //                       nuclide bisection of the SoA energy column.
@@ -165,7 +165,7 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
 template <int GT>
 __device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
   if (GT == GF_GRID_UNIONIZED) {
-    // #{U <= E} lies in [ubin[b], ubin[b+1]] for b = floor(E 2^14) (ubin[2^14] = n covers E >= 1).
+    // #{U <= E} lies in [ubin[b], ubin[b+1]] for b = floor(E 2^20) (ubin[2^20] = n covers E >= 1).
     const int b = energy_bin(E);
     long long lo = __ldg(X.ubin + b), hi = __ldg(X.ubin + b + 1);
     if (b == kUBins - 1) hi = X.n_union;

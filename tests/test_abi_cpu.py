@@ -95,7 +95,7 @@ def test_grid_bytes_closed_form():
         want = al(npts * 48) + al(npts * 8) + al(npts * 8) + al(16)  # G, Ed, reciprocal widths, flags
         if gt == gf.UNIONIZED:
             pitch = (npts + 63) // 64 * 64
-            want += al(npts * 8) + al(n_iso * pitch * 2) + al(16385 * 4)
+            want += al(npts * 8) + al(n_iso * pitch * 2) + al((2 ** 20 + 1) * 4)
         if gt != gf.NUCLIDE:
             want += al(npts * 128)  # interval records of the sorted kernel
         if gt == gf.HASH:

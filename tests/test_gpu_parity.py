@@ -99,7 +99,7 @@ def check_arrays(o, g, full_ig=True):
         U = g.array("unionized")[0].cpu().numpy()
         assert np.array_equal(U, o.unionized())
         ub = g.array("union_bins")[0].cpu().numpy().astype(np.int64)
-        edges = np.arange(16385) / 16384.0
+        edges = np.arange(2 ** 20 + 1) / 2.0 ** 20
         want_ub = np.searchsorted(o.unionized(), edges, side="left")
         want_ub[-1] = len(U)
         assert np.array_equal(ub, want_ub)

@@ -9,8 +9,9 @@ the rank's shard of the config's event lookups: sample -> locality sort -> searc
 accumulate -> hash reduction, then the cross-rank int64 all-reduce of the raw hash (NCCL) when
 N > 1.  The grid build (A0) runs once before timing and is reported separately (grid_build_ms),
 like the paper's kernel-only timing.  Default workload: C3 = XSBench large,
-unionized grid, 17 M lookups (BASELINE.json configs[2], the north_star's target), strong-scaled
-over N ranks.  Every step is timed with CUDA events on the launching stream; L2 is flushed by a
+unionized grid, 17 M lookups (BASELINE.json configs[2], the north_star's target), weak-scaled
+over N ranks by default (every rank runs 17 M lookups from its own global index range; --scaling
+strong splits the 17 M instead).  Every step is timed with CUDA events on the launching stream; L2 is flushed by a
 256 MiB write between steps (outside the events).  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
@@ -188,7 +189,7 @@ def run_reference(args, rank, world):
     v = step_n * args.steps / tot
     line = {"impl": "reference", "metric": "lookups/sec", "value": v, "unit": "lookups/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
             "config": {"workload": f"{cfg_name}: {desc}", "n_lookups": n, "step_sample": step_n},
             "cpu_baseline": {"value": v, "unit": "lookups/s", "cores": threads, "kind": "oracle",
@@ -204,6 +205,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs the config's lookups (global indices [r n, (r+1) n)); "
+                         "strong: the config's lookups are split over the ranks")
     ap.add_argument("--no-sort", action="store_true", help="skip the A2 locality sort (unsorted gather kernel)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -233,7 +237,11 @@ def main():
         dist.barrier()
     dev = torch.device("cuda", local)
     bench, n_iso, gt, n_total, desc = CONFIGS[args.config]
-    first, n = gf.shard_range(n_total, rank, world)
+    if args.scaling == "weak":
+        first, n = gf.weak_range(n_total, rank)
+        n_total = n * world
+    else:
+        first, n = gf.shard_range(n_total, rank, world)
     st = torch.cuda.current_stream()
 
     # ---------------------------------------------------------------- A0: grid build (untimed)
@@ -372,11 +380,12 @@ def main():
         clk = clocks.summary()
         line = {
             "metric": "lookups/sec", "value": value, "unit": "lookups/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
             "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n,
                        "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
-                       "parallelism": f"lookup shards x{world}, grid replicated, 1 int64 "
+                       "parallelism": f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, {first + n}) on rank 0), "
+                                      f"grid replicated, 1 int64 "
                                       f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
             "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": K * launches_per_step(bench, gt, flags),

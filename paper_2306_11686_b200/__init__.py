@@ -17,7 +17,7 @@ import os
 from .build import LIB as _LIB_PATH
 
 __all__ = ["Params", "Grid", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
-           "SORT_LOCALITY", "HISTORY", "HOST_IO", "HASH_MOD", "STARTING_SEED", "shard_range", "GFError"]
+           "SORT_LOCALITY", "HISTORY", "HOST_IO", "HASH_MOD", "STARTING_SEED", "shard_range", "weak_range", "GFError"]
 
 XSBENCH, RSBENCH = 0, 1
 NUCLIDE, UNIONIZED, HASH = 0, 1, 2
@@ -118,6 +118,13 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Rank r of W takes the contiguous global indices [floor(r n / W), floor((r+1) n / W))."""
     lo, hi = (rank * n) // world, ((rank + 1) * n) // world
     return lo, hi - lo
+
+
+def weak_range(n_per_rank: int, rank: int) -> tuple[int, int]:
+    """Weak scaling: rank r takes the global indices [r n, (r+1) n) -- every rank does the config's
+    single-GPU workload, the ranks' ranges are disjoint and consecutive, so the union over W ranks is
+    the event batch [0, W n) and the all-reduced raw sum is that batch's."""
+    return rank * n_per_rank, n_per_rank
 
 
 def _stream_ptr(torch, stream):

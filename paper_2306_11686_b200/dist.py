@@ -4,9 +4,9 @@ of the raw verification sum per batch.  Works with any torch.distributed backend
 box; gloo in the CPU tests)."""
 from __future__ import annotations
 
-from . import shard_range, verify
+from . import shard_range, verify, weak_range
 
-__all__ = ["shard_range", "reduce_raw", "max_over_ranks", "finish_hash"]
+__all__ = ["shard_range", "weak_range", "reduce_raw", "max_over_ranks", "finish_hash"]
 
 
 def reduce_raw(vsum, group=None):

@@ -55,3 +55,15 @@ def test_gloo_sharded_hash_equals_single_process(world):
     assert raw == full
     assert h == gf.verify(full)
     assert t == [2.0, 10.0]
+
+
+def test_weak_ranges_tile_the_batch():
+    """Weak scaling (bench default): rank r of W runs [r n, (r+1) n); the ranges tile [0, W n), so the
+    all-reduced raw sum of W ranks is the raw sum of one W n batch (hash additivity)."""
+    import oracle as O
+    import paper_2306_11686_b200 as gf
+    n, world = 997, 3
+    rs = [gf.weak_range(n, r) for r in range(world)]
+    assert [f for f, _ in rs] == [0, n, 2 * n] and all(c == n for _, c in rs)
+    o = O.XSOracle(68, 11303, O.NUCLIDE)
+    assert sum(o.lookup_batch(f, c, threads=1) for f, c in rs) == o.lookup_batch(0, world * n, threads=1)

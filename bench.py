@@ -35,12 +35,15 @@ CONFIGS = {
     "C3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized grid, 17M event lookups"),
     "C4": ("xs", 355, 2, 170_000_000, "XSBench large 355x11303, hash grid 10000 bins, 170M event lookups"),
     "C5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, windowed multipole + Faddeeva, 10.2M lookups"),
+    # NEXT-3: the nuclide grid at scale -- not a BASELINE.json config
+    "C3N": ("xs", 355, 0, 17_000_000, "XSBench large 355x11303, nuclide-grid search, 17M event lookups (NEXT-3)"),
 }
 # Per-lookup algorithmic work of the dominant kernel:
 #   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
 #   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
 #   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop).
-ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000)}
+ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
+       "C3N": (0, 1551)}
 
 
 def launches_per_step(bench, gt, sorted_):
@@ -353,7 +356,7 @@ def main():
         elif not flags:
             kname = f"xs_lookup_direct<{gname}>"
         elif gt == 0:
-            kname = "xs_lookup_sorted<nuclide>"
+            kname = "xs_lookup_warp_nuclide (warp-cooperative search)"
         else:
             kname = f"xs_lookup_group<{gname}> (+ idx_prep, ~1% of the stage)"
         flops = alg_flops * per_launch_lookups

@@ -391,11 +391,13 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 
 // ------------------------------------------------------------------------------------------ production
 #include "xs_sorted_u.cuh"
+#include "xs_warp_nuclide.cuh"
 
 // Kernel for the sorted path.  GF_XS_KERNEL in the environment selects an alternative for A/B
 // measurements: "staged" (TMA producer/consumer ring, unionized only), "thread" (non-persistent,
-// one lookup per thread); default "group" (persistent, kL lookups per thread; unionized and hash
-// grids).  All give identical results.
+// one lookup per thread, per-lane bisection on the nuclide grid); default "group" (persistent, kL
+// lookups per thread; unionized and hash grids) and, on the nuclide grid, the warp-cooperative
+// search kernel.  All give identical results.
 enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2 };
 static int sorted_kernel() {
   static int v = -1;
@@ -424,6 +426,11 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if (GT != GF_GRID_NUCLIDE && sorted_kernel() != kKernThread)
       return X.fastdiv ? launch_group<GT, true>(X, n, S, macro_out, vsum, st)
                        : launch_group<GT, false>(X, n, S, macro_out, vsum, st);
+    if (GT == GF_GRID_NUCLIDE && sorted_kernel() != kKernThread) {
+      xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out,
+                                                                           vsum);
+      return cudaGetLastError();
+    }
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;

@@ -217,8 +217,8 @@ def test_C2_small_unionized(gf):
     assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
 
 
-@pytest.mark.parametrize("kernel", ["staged", "thread"])
-def test_alternative_sorted_kernels_match(gf, kernel):
+@pytest.mark.parametrize("kernel,grid", [("staged", 1), ("thread", 1), ("thread", 0)])
+def test_alternative_sorted_kernels_match(gf, kernel, grid):
     """GF_XS_KERNEL selects the alternative kernels of the sorted unionized path (the TMA-staged
     producer/consumer ring, the non-persistent per-thread kernel); they must give the oracle's bits
     too (run in a child process: the switch is read once)."""
@@ -226,7 +226,7 @@ def test_alternative_sorted_kernels_match(gf, kernel):
     import sys
     code = (
         "import numpy as np, oracle as O, paper_2306_11686_b200 as gf\n"
-        "o = O.XSOracle(355, 11303, O.UNIONIZED); g = gf.Grid(gf.Params.xsbench(355, 11303, gf.UNIONIZED))\n"
+        f"o = O.XSOracle(355, 11303, {grid}); g = gf.Grid(gf.Params.xsbench(355, 11303, {grid}))\n"
         "r1, m1 = o.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
         "r2, m2 = g.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
         "assert r1 == r2 and np.array_equal(m1, m2.cpu().numpy())\n"
@@ -354,6 +354,36 @@ def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
         raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
         assert raw_g == raw_o
         assert np.array_equal(m_g.cpu().numpy(), m_o), f"mat {mat}"
+
+
+def test_nuclide_warp_search_edges(gf, torch):
+    """The nuclide-grid sorted kernel searches once per warp (32-ary warp-cooperative search over the
+    warp's [Emin, Emax], then a shuffle search per lane).  Exact gridpoints and their 1-ulp
+    neighbours inside one warp, dense clusters (narrow warps), a sparse spread (wide warps that end
+    in the per-lane fallback), the grid ends, energies outside [0, 1], +-inf and NaN (which takes
+    grid_search's per-lane path) must all give the oracle's bits."""
+    o, g = make_pair(gf, 68, 11303, O.NUCLIDE)
+    rng = np.random.default_rng(5)
+    G = o.nuclide_grid()
+    Es = []
+    for nuc in (0, 2, 41, 67):
+        for k in list(rng.integers(0, o.n_gp - 1, 8)) + [0, 1, o.n_gp - 2, o.n_gp - 1]:
+            e = float(G[nuc, k, 0])
+            Es += [e, math.nextafter(e, -1), math.nextafter(e, 2), e] + list(e + (rng.random(12) - 0.5) * 1e-6)
+    Es += list(0.25 + rng.random(3000) * 1e-4)            # narrow warps
+    Es += list(rng.random(40))                             # wide warps
+    Es += [0.0, 1.0, -0.5, 3.0, math.inf, -math.inf, 5e-324, -0.0]
+    E = np.array(Es)
+    for mat in (0, 4, 7):
+        for extra in ([], [math.nan, math.nan, 0.5]):
+            EE = np.concatenate([E, np.array(extra, dtype=np.float64)])
+            mats = np.full(len(EE), mat, dtype=np.uint8)
+            raw_o, m_o = o.lookup_energies(EE, mats.astype(np.int32))
+            raw_g, m_g = g.lookup_energies(torch.from_numpy(EE).cuda(), torch.from_numpy(mats).cuda(), sort=True)
+            m_g = m_g.cpu().numpy()
+            assert raw_g == raw_o
+            fin = ~np.isnan(m_o)
+            assert np.array_equal(np.isnan(m_g), ~fin) and np.array_equal(m_g[fin], m_o[fin]), f"mat {mat}"
 
 
 def test_host_io_pipeline_chunks(gf, torch):

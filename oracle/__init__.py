@@ -80,6 +80,8 @@ def lib():
         L.rso_macro.restype = None; L.rso_macro.argtypes = [vp, dbl, i32, vp, P(dbl)]
         L.rso_lookup_batch.restype = u64; L.rso_lookup_batch.argtypes = [vp, u64, u64, u64, vp, vp, i32]
         L.rso_lookup_indices.restype = u64; L.rso_lookup_indices.argtypes = [vp, vp, u64, u64, vp, vp]
+        L.xso_history_batch.restype = u64; L.xso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, i32]
+        L.rso_history_batch.restype = u64; L.rso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, vp, i32]
         _lib = L
     return _lib
 
@@ -237,6 +239,14 @@ class XSOracle:
         raw = lib().xso_lookup_indices(self.h, _ptr(idx), len(idx), seed, _ptr(out))
         return raw, out
 
+    def history_batch(self, first_p: int, n_p: int, L: int = 34, seed: int = STARTING_SEED, want_macro=False,
+                      threads=0):
+        """History-based mode (NEXT-1, reading R-HIST): particles [first_p, first_p + n_p), L lookups each.
+        Returns raw (and macro [n_p][L][5])."""
+        out = np.zeros((n_p, L, 5), dtype=np.float64) if want_macro else None
+        raw = lib().xso_history_batch(self.h, first_p, n_p, L, seed, _ptr(out), threads)
+        return (raw, out) if want_macro else raw
+
     def lookup_energies(self, E, mat):
         E = np.ascontiguousarray(E, dtype=np.float64)
         mat = np.ascontiguousarray(mat, dtype=np.int32)
@@ -293,3 +303,11 @@ class RSOracle:
         sc = np.zeros(len(idx))
         raw = lib().rso_lookup_indices(self.h, _ptr(idx), len(idx), seed, _ptr(out), _ptr(sc))
         return raw, out, sc
+
+    def history_batch(self, first_p: int, n_p: int, L: int = 34, seed: int = STARTING_SEED, want_macro=False,
+                      threads=0):
+        """History-based mode (NEXT-1, reading R-HIST-RS).  Returns raw (and macro [n_p][L][4], S [n_p][L])."""
+        out = np.zeros((n_p, L, 4)) if want_macro else None
+        sc = np.zeros((n_p, L)) if want_macro else None
+        raw = lib().rso_history_batch(self.h, first_p, n_p, L, seed, _ptr(out), _ptr(sc), threads)
+        return (raw, out, sc) if want_macro else raw

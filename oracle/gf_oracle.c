@@ -20,6 +20,9 @@
  * Parity status per function:
  *   o_lcg_*, o_fast_forward, o_thresholds, o_pick_mat, xs grid build, grid_search, ig/hg entries,
  *   xs lookups, RS Faddeeva constants: pinned (tests/test_oracle_*.py).
+ *   xso_history_batch / rso_history_batch (NEXT-1): pinned by the L = 1 reduction to event lookups,
+ *   an independent Python transcription of the particle chain (exact-integer LCG, per-step macro
+ *   from the pinned xso_macro / rso_macro) and hash bounds / additivity (tests/test_oracle_history.py).
  *   Results vs the real XSBench/RSBench binaries: parity unpinned (no implementation exists to
  *   compare against; SURVEY.md:691).  RS generator layout: pinned only to the survey's reading
  *   (golden values SURVEY.md:996-997).
@@ -415,6 +418,44 @@ uint64_t xso_lookup_energies(const xs_oracle *o, const double *E, const int *mat
     return raw;
 }
 
+/* History-based mode (NEXT-1; "event-based lookup and
+ * history-based lookup"; reading R-HIST, SURVEY.md:679 and DESIGN.md Sec. 3).  Particle p (GLOBAL
+ * index) runs L dependent lookups:
+ *     s = fast_forward(seed, p * L * 2 * 4);  E = lcg_double(&s);  mat = pick_mat(lcg_double(&s))
+ *     for i in 0 .. L-1:
+ *         macro = lookup(E, mat);  raw += 1 + argmax(macro)
+ *         n_forward = #{c : macro[c] > 1.0};  if n_forward > 0: s = fast_forward(s, n_forward)
+ *         E = lcg_double(&s);  mat = pick_mat(lcg_double(&s))
+ * Particles [first_p, first_p + n_p).  macro_out: NULL or [n_p][L][5].  Returns the exact raw sum. */
+uint64_t xso_history_batch(const xs_oracle *o, uint64_t first_p, uint64_t n_p, int L, uint64_t seed,
+                           double *macro_out, int nthreads) {
+    uint64_t raw = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : raw)
+    for (long long t = 0; t < (long long)n_p; t++) {
+        uint64_t p = first_p + (uint64_t)t;
+        uint64_t s = o_fast_forward(seed, p * (uint64_t)L * 2ULL * 4ULL);
+        double E = o_lcg_double(&s);
+        int mat = o_pick_mat(o_lcg_double(&s));
+        for (int i = 0; i < L; i++) {
+            double macro[5];
+            xso_macro(o, E, mat, macro);
+            raw += (uint64_t)o_argmax5_plus1(macro);
+            if (macro_out)
+                for (int c = 0; c < 5; c++) macro_out[((size_t)t * L + i) * 5 + c] = macro[c];
+            uint64_t n_forward = 0;
+            for (int c = 0; c < 5; c++)
+                if (macro[c] > 1.0) n_forward++;
+            if (n_forward > 0) s = o_fast_forward(s, n_forward);
+            E = o_lcg_double(&s);
+            mat = o_pick_mat(o_lcg_double(&s));
+        }
+    }
+    return raw;
+}
+
 /* ================================================================ RSBench (SURVEY.md:594-633) */
 typedef struct {
     double r, i;
@@ -708,6 +749,41 @@ uint64_t rso_lookup_indices(const rs_oracle *o, const uint64_t *idx, uint64_t n,
         if (macro_out)
             for (int c = 0; c < 4; c++) macro_out[(size_t)t * 4 + c] = macro[c];
         if (scale_out) scale_out[t] = S;
+    }
+    return raw;
+}
+
+/* RSBench history-based mode (NEXT-1; reading R-HIST-RS).  Particle p (GLOBAL
+ * index) runs L dependent lookups:
+ *     s = fast_forward(seed, p * L * 2);  E = lcg_double(&s);  mat = pick_mat(lcg_double(&s))
+ *     for i in 0 .. L-1:
+ *         macro = lookup(E, mat);  raw += 1 + argmax4(macro)
+ *         for x in 0..3: s += (macro[x] > 0) ? 1337 * p : 42          (u64 wraparound)
+ *         E = lcg_double(&s);  mat = pick_mat(lcg_double(&s))
+ * macro_out: NULL or [n_p][L][4]; scale_out: NULL or [n_p][L] (the R-UNIQ scale S). */
+uint64_t rso_history_batch(const rs_oracle *o, uint64_t first_p, uint64_t n_p, int L, uint64_t seed,
+                           double *macro_out, double *scale_out, int nthreads) {
+    uint64_t raw = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : raw)
+    for (long long t = 0; t < (long long)n_p; t++) {
+        uint64_t p = first_p + (uint64_t)t;
+        uint64_t s = o_fast_forward(seed, p * (uint64_t)L * 2ULL);
+        double E = o_lcg_double(&s);
+        int mat = o_pick_mat(o_lcg_double(&s));
+        for (int i = 0; i < L; i++) {
+            double macro[4], S;
+            rso_macro(o, E, mat, macro, &S);
+            raw += (uint64_t)o_argmax4_plus1(macro);
+            if (macro_out)
+                for (int c = 0; c < 4; c++) macro_out[((size_t)t * L + i) * 4 + c] = macro[c];
+            if (scale_out) scale_out[(size_t)t * L + i] = S;
+            for (int x = 0; x < 4; x++) s += (macro[x] > 0.0) ? 1337ULL * p : 42ULL;
+            E = o_lcg_double(&s);
+            mat = o_pick_mat(o_lcg_double(&s));
+        }
     }
     return raw;
 }

@@ -37,13 +37,26 @@ CONFIGS = {
     "C5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, windowed multipole + Faddeeva, 10.2M lookups"),
     # NEXT-3: the nuclide grid at scale -- not a BASELINE.json config
     "C3N": ("xs", 355, 0, 17_000_000, "XSBench large 355x11303, nuclide-grid search, 17M event lookups (NEXT-3)"),
+    # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
+    "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
+    "H3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
+    "H5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, HISTORY mode 300k particles x 34 lookups"),
 }
+HIST_L = {"H2": 34, "H3": 34, "H5": 34}  # lookups per particle (history configs)
 # Per-lookup algorithmic work of the dominant kernel:
 #   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
 #   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
 #   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop).
 ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
-       "C3N": (0, 1551)}
+       "C3N": (0, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
+
+
+def oracle_run(o, cfg, first, n, threads):
+    """The oracle on lookups [first, first + n) of a config (history configs: whole particles)."""
+    L = HIST_L.get(cfg)
+    if L:
+        return o.history_batch(first // L, max(1, n // L), L, threads=threads), max(1, n // L) * L
+    return o.lookup_batch(first, n, threads=threads), n
 
 
 def launches_per_step(bench, gt, sorted_):
@@ -154,11 +167,11 @@ def cpu_baseline(cfg_name, seconds=12.0):
         o = O.RSOracle(n_iso, 1000, 100, 4)
     k = 20_000
     t = time.perf_counter()
-    o.lookup_batch(0, k, threads=threads)
+    _, k = oracle_run(o, cfg_name, 0, k, threads)
     dt = time.perf_counter() - t
     k2 = int(min(n, max(k, k * seconds / max(dt, 1e-6))))
     t = time.perf_counter()
-    o.lookup_batch(0, k2, threads=threads)
+    _, k2 = oracle_run(o, cfg_name, 0, k2, threads)
     dt = time.perf_counter() - t
     return {"value": k2 / dt, "unit": "lookups/s", "cores": threads, "kind": "oracle",
             "sample": f"global lookup indices [0, {k2}) of {cfg_name} ({k2 / n:.2%} of the workload), "
@@ -175,17 +188,19 @@ def run_reference(args, rank, world):
     threads = len(os.sched_getaffinity(0))
     o = O.XSOracle(n_iso, 11303, gt, bins=10000) if bench == "xs" else O.RSOracle(n_iso, 1000, 100, 4)
     t = time.perf_counter()
-    o.lookup_batch(0, 20_000, threads=threads)
-    per = (time.perf_counter() - t) / 20_000
+    _, k0 = oracle_run(o, cfg_name, 0, 20_000, threads)
+    per = (time.perf_counter() - t) / k0
     step_n = int(max(20_000, min(n, 2.0 / max(per, 1e-9))))  # ~2 s of CPU per step
     first = 0
+    HLr = HIST_L.get(cfg_name, 1)
+    step_n = HLr * max(1, step_n // HLr)  # history configs: whole particles
     for _ in range(args.warmup):
-        o.lookup_batch(first, step_n, threads=threads)
+        oracle_run(o, cfg_name, first, step_n, threads)
         first = (first + step_n) % max(1, n - step_n)
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        o.lookup_batch(first, step_n, threads=threads)
+        oracle_run(o, cfg_name, first, step_n, threads)
         times.append(time.perf_counter() - t)
         first = (first + step_n) % max(1, n - step_n)
     tot = sum(times)
@@ -212,6 +227,8 @@ def main():
                     help="weak: every rank runs the config's lookups (global indices [r n, (r+1) n)); "
                          "strong: the config's lookups are split over the ranks")
     ap.add_argument("--no-sort", action="store_true", help="skip the A2 locality sort (unsorted gather kernel)")
+    ap.add_argument("--hist-mode", default="sorted", choices=["sorted", "waves", "direct"],
+                    help="history configs: sorted step waves (default), unsorted waves, or one thread per particle")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -220,6 +237,8 @@ def main():
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+
+    import ctypes as C
 
     import torch
     import paper_2306_11686_b200 as gf
@@ -257,10 +276,17 @@ def main():
     grid_ms = e0.elapsed_time(e1)
 
     flags = 0 if args.no_sort else gf.SORT_LOCALITY
-    scratch = torch.empty(grid.scratch_bytes(n, flags), dtype=torch.uint8, device=dev)
+    HL = HIST_L.get(args.config)
+    if HL:  # history mode: the unit of work is a particle (HL dependent lookups)
+        flags = gf.Grid.HIST_MODES[args.hist_mode]
+        np_first, n_part = first // HL, n // HL
+        hb = C.c_size_t()
+        gf._check(gf.lib().gf_xs_history_bytes(grid.h, n_part, flags, C.byref(hb)))
+        scratch = torch.empty(max(hb.value, 256), dtype=torch.uint8, device=dev)
+    else:
+        scratch = torch.empty(grid.scratch_bytes(n, flags), dtype=torch.uint8, device=dev)
     vsum = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    import ctypes as C
     L = gf.lib()
 
     K = args.steps
@@ -269,6 +295,17 @@ def main():
     def step(k):
         ev = evs[k]
         vsum.zero_()
+        if HL:  # one gf_xs_history_batch call: HL waves (or one direct kernel)
+            ev[0].record()
+            ev[1].record()
+            gf._check(L.gf_xs_history_batch(grid.h, np_first, n_part, HL, gf.STARTING_SEED, flags, None,
+                                            C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                            scratch.numel(), C.c_void_p(st.cuda_stream)))
+            ev[2].record()
+            if dist is not None:
+                dist.all_reduce(vsum)
+            ev[3].record()
+            return
         se = (C.c_void_p * 3)(ev[0].cuda_event, ev[1].cuda_event, ev[2].cuda_event)
         gf._check(L.gf_xs_lookup_batch_ev(grid.h, first, n, gf.STARTING_SEED, flags, None,
                                           C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
@@ -315,7 +352,26 @@ def main():
 
     # ---------------------------------------------------------------- end-to-end through the public API
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and HL:  # history: no per-step inputs (indices + seed); the raw sum comes back
+        reps = 3
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r_e2e = grid.history_batch(np_first, n_part, HL, mode=args.hist_mode)
+            if dist is not None:
+                rt = torch.tensor([r_e2e], dtype=torch.int64, device=dev)
+                dist.all_reduce(rt)
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = t.item()
+        e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
+               "path": "Grid.history_batch (gf_xs_history_batch): particle indices + seed in, raw sum (8 B) out; "
+                       "host-timed incl. launch and sync"}
+    elif not args.no_e2e:
         import numpy as np
         rng = np.random.default_rng(1234 + rank)
         P = np.array([0.139, 0.052, 0.275, 0.134, 0.154, 0.064, 0.066, 0.055, 0.008, 0.015, 0.025, 0.013])
@@ -359,6 +415,10 @@ def main():
             kname = "xs_lookup_warp_nuclide (warp-cooperative search)"
         else:
             kname = f"xs_lookup_group<{gname}> (+ idx_prep, ~1% of the stage)"
+        if HL:
+            kname = ({"direct": f"{bench}_history_direct (one thread per particle, {HL} dependent lookups)"}.get(
+                args.hist_mode, f"{HL} waves of hist_sample + " + ("sort + " if flags & gf.SORT_LOCALITY else "")
+                + kname) + "; stage = the whole history call")
         flops = alg_flops * per_launch_lookups
         prof = load_profile(args.config, not args.no_sort)
         roof = {"bound": "alu", "kernel": kname,
@@ -386,12 +446,16 @@ def main():
             "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
             "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n,
+                       **({"mode": f"history ({args.hist_mode})", "particles_per_rank": n_part,
+                           "lookups_per_particle": HL} if HL else {}),
                        "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
                        "parallelism": f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, {first + n}) on rank 0), "
                                       f"grid replicated, 1 int64 "
                                       f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
             "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": K * launches_per_step(bench, gt, flags),
+            "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY) if not HL else
+                                 (1 if args.hist_mode == "direct" else
+                                  HL * (1 + launches_per_step(bench, gt, flags & gf.SORT_LOCALITY)))),
             "clocks": clk,
             "stage_ms": {"sort": statistics.median(sort_ms), "lookup": statistics.median(look_ms),
                          "step": statistics.median(step_ms), "grid_build": grid_ms},

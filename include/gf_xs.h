@@ -129,10 +129,14 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 enum {
     GF_SORT_LOCALITY = 1u << 0, /* A2: bin lookups by (material, energy) before the lookup kernel
                                    (default in bench).  Results are identical either way. */
-    GF_HISTORY = 1u << 1,       /* NEXT-1 history-based mode: GF_E_UNSUPPORTED in ABI v1 */
-    GF_HOST_IO = 1u << 2        /* outputs (and, for gf_xs_lookup_energies, inputs) are HOST
+    GF_HISTORY = 1u << 1,       /* history-based mode is a separate call (gf_xs_history_batch): in
+                                   the event-lookup calls this flag returns GF_E_UNSUPPORTED */
+    GF_HOST_IO = 1u << 2,       /* outputs (and, for gf_xs_lookup_energies, inputs) are HOST
                                    pointers; the call stages them through `scratch`, copies inside
                                    the call and synchronises `stream` before returning */
+    GF_HIST_WAVES = 1u << 3     /* gf_xs_history_batch: run step i of all particles as one event-style
+                                   batch (implied by GF_SORT_LOCALITY); without it, one thread per
+                                   particle runs its L lookups back to back */
 };
 
 /* Scratch bytes a lookup call of n lookups with `flags` needs (caller allocates on the device). */
@@ -171,6 +175,30 @@ gf_status gf_xs_lookup_batch_ev(const gf_xs_grid *g, uint64_t first, uint64_t n,
 gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint8_t *mat, uint64_t n, uint32_t flags,
                                 double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
                                 gf_stream_t stream);
+
+/* NEXT-1: HISTORY-BASED lookups, PAPER.md:1408 ("event-based lookup and
+ * history-based lookup").  Particles with GLOBAL indices [first_particle, first_particle + n_particles)
+ * each run `lookups_per_particle` (L, 34 in XSBench / RSBench) DEPENDENT lookups; the readings
+ * are
+ *   XSBench (R-HIST):    s = fast_forward(seed, 8 L p); E, mat drawn; after each lookup
+ *                        s = fast_forward(s, #{c : macro_c > 1.0}), then E, mat drawn again.
+ *   RSBench (R-HIST-RS): s = fast_forward(seed, 2 L p); E, mat drawn; after each lookup
+ *                        s += (macro_c > 0 ? 1337 p : 42) for c = 0..3 (u64), then E, mat drawn.
+ * flags: 0 = one thread per particle (GPU First's mapping of the particle loop); GF_HIST_WAVES =
+ * step-synchronous waves of n_particles event lookups; GF_SORT_LOCALITY (implies waves) = waves with
+ * the A2 locality sort.  Results are identical in every mode.
+ *   d_macro_out: NULL, or fp64 [n_particles][L][5] (XS) / [n_particles][L][4] (RS), row
+ *                (p - first_particle) * L + i.
+ *   d_vsum:      uint64; the call ADDS sum(1 + argmax) over all n_particles * L lookups.
+ * n_particles < 2^32, 1 <= L <= 2^20.  Enqueued on `stream`; scratch from gf_xs_history_bytes.
+ * (RSBench: the sign test macro_c > 0 decides the stream.  The RS macro xs agree with the oracle to
+ * 1e-10 S (R-UNIQ), so a channel within that distance of 0 could branch differently; the parity
+ * tests report the smallest |macro_c| / S seen.) */
+gf_status gf_xs_history_bytes(const gf_xs_grid *g, uint64_t n_particles, uint32_t flags, size_t *scratch_bytes);
+gf_status gf_xs_history_batch(const gf_xs_grid *g, uint64_t first_particle, uint64_t n_particles,
+                              int32_t lookups_per_particle, uint64_t starting_seed, uint32_t flags,
+                              double *d_macro_out, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                              gf_stream_t stream);
 
 /* Grid facts: *fastdiv = 1 when the lookup kernels use the exact reciprocal division (every
  * interval of the nuclide grid has a normal, non-zero width), 0 when they use __ddiv_rn. */

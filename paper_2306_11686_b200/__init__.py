@@ -17,11 +17,11 @@ import os
 from .build import LIB as _LIB_PATH
 
 __all__ = ["Params", "Grid", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
-           "SORT_LOCALITY", "HISTORY", "HOST_IO", "HASH_MOD", "STARTING_SEED", "shard_range", "weak_range", "GFError"]
+           "SORT_LOCALITY", "HISTORY", "HOST_IO", "HIST_WAVES", "HASH_MOD", "STARTING_SEED", "shard_range", "weak_range", "GFError"]
 
 XSBENCH, RSBENCH = 0, 1
 NUCLIDE, UNIONIZED, HASH = 0, 1, 2
-SORT_LOCALITY, HISTORY, HOST_IO = 1, 2, 4
+SORT_LOCALITY, HISTORY, HOST_IO, HIST_WAVES = 1, 2, 4, 8
 HASH_MOD = 999983
 STARTING_SEED = 1070
 ABI_VERSION = 1
@@ -85,6 +85,8 @@ def lib():
             "gf_xs_lookup_batch": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_lookup_batch_ev": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp, vp]),
             "gf_xs_lookup_energies": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, vp, sz, vp]),
+            "gf_xs_history_bytes": (i32, [vp, u64, C.c_uint32, P(sz)]),
+            "gf_xs_history_batch": (i32, [vp, u64, u64, i32, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_verify": (i32, [u64, u64, P(u64)]),
             "gf_xs_grid_info": (i32, [vp, P(i32)]),
             "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
@@ -265,5 +267,33 @@ class Grid:
         _check(lib().gf_xs_lookup_energies(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()), n, flags,
                                            C.c_void_p(macro.data_ptr()) if want_macro else None,
                                            C.c_void_p(vsum.data_ptr()), C.c_void_p(sc.data_ptr()), sc.numel(), st))
+        raw = int(vsum.item())
+        return (raw, macro) if want_macro else raw
+
+    # ----------------------------------------------------------------- history mode (NEXT-1)
+    HIST_MODES = {"direct": 0, "waves": HIST_WAVES, "sorted": HIST_WAVES | SORT_LOCALITY}
+
+    def history_batch_async(self, first_p: int, n_p: int, vsum, L: int = 34, seed: int = STARTING_SEED,
+                            mode: str = "sorted", macro_out=None, stream=None):
+        """Enqueue particles [first_p, first_p + n_p), L dependent lookups each (gf_xs_history_batch);
+        ADDS the raw sum to the int64 device tensor `vsum`.  mode: "sorted" (waves + locality sort),
+        "waves" or "direct" (one thread per particle)."""
+        flags = self.HIST_MODES[mode]
+        b = C.c_size_t()
+        _check(lib().gf_xs_history_bytes(self.h, n_p, flags, C.byref(b)))
+        if self._scratch is None or self._scratch.numel() < b.value:
+            self._scratch = self.torch.empty(b.value, dtype=self.torch.uint8, device=self.device)
+        sc = self._scratch
+        mo = C.c_void_p(macro_out.data_ptr()) if macro_out is not None else None
+        _check(lib().gf_xs_history_batch(self.h, first_p, n_p, L, seed, flags, mo, C.c_void_p(vsum.data_ptr()),
+                                         C.c_void_p(sc.data_ptr()), sc.numel(), _stream_ptr(self.torch, stream)))
+
+    def history_batch(self, first_p: int, n_p: int, L: int = 34, seed: int = STARTING_SEED, mode: str = "sorted",
+                      want_macro: bool = False, stream=None):
+        """History-based lookups -> raw sum (int), and the [n_p][L][5|4] fp64 macro xs if asked."""
+        torch = self.torch
+        vsum = torch.zeros(1, dtype=torch.int64, device=self.device)
+        macro = torch.empty((n_p, L, self.channels), dtype=torch.float64, device=self.device) if want_macro else None
+        self.history_batch_async(first_p, n_p, vsum, L, seed, mode, macro, stream)
         raw = int(vsum.item())
         return (raw, macro) if want_macro else raw

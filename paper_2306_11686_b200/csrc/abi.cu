@@ -475,8 +475,8 @@ static cudaError_t launch_lookup(const gf_xs_grid *g, uint64_t first, uint32_t n
                                  const uint8_t *dmat, bool sort, const SortScratch &S, double *dmacro,
                                  unsigned long long *dvsum, cudaStream_t st, cudaEvent_t ev_mid) {
   return g->p.bench == GF_XSBENCH
-             ? launch_xs_lookup(g->xs, first, n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid)
-             : launch_rs_lookup(g->rs, first, n, seed, dE, dmat, sort, S, dmacro, dvsum, st, ev_mid);
+             ? launch_xs_lookup(g->xs, first, n, seed, dE, dmat, sort, S, out_macro(dmacro, 5), dvsum, st, ev_mid)
+             : launch_rs_lookup(g->rs, first, n, seed, dE, dmat, sort, S, out_macro(dmacro, 4), dvsum, st, ev_mid);
 }
 
 // Internal streams / events of the host-IO pipeline (created on first use, per grid).
@@ -544,7 +544,7 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
                             size_t scratch_bytes, gf_stream_t stream, const gf_stage_events *ev = nullptr) {
   if (!g) return fail(GF_E_INVAL, "grid is NULL");
   if (!vsum) return fail(GF_E_INVAL, "vsum is NULL");
-  if (flags & GF_HISTORY) return fail(GF_E_UNSUPPORTED, "history-based mode is NEXT-1 (not built in ABI v1)");
+  if (flags & GF_HISTORY) return fail(GF_E_UNSUPPORTED, "history-based mode is gf_xs_history_batch");
   if (flags & ~(uint32_t)(GF_SORT_LOCALITY | GF_HISTORY | GF_HOST_IO)) return fail(GF_E_INVAL, "unknown flags 0x%x", flags);
   if (n >= (1ull << 32)) return fail(GF_E_INVAL, "n = %llu >= 2^32: split the job into batches", (unsigned long long)n);
   const bool energies = E != nullptr;
@@ -604,6 +604,100 @@ gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint
     static const uint8_t kDummyMat = 0;
     return run_lookup(g, 0, n, 0, E ? E : &kDummy, mat ? mat : (n ? nullptr : &kDummyMat), flags, macro_out, vsum,
                       scratch, scratch_bytes, stream);
+  } catch (...) {
+    return fail(GF_E_NOMEM, "host allocation failed");
+  }
+}
+
+// ------------------------------------------------------------------------------------------ history (NEXT-1)
+// Waves scratch: per particle the LCG state (8 B), this wave's E (8 B) and material (1 B), the
+// feedback byte of the previous wave, then one sort slot for n_particles lookups.
+struct HistLayout {
+  size_t state, Ep, matp, fb, slot, total;
+  BatchLayout B;
+};
+
+static void plan_history(const gf_xs_grid *g, uint64_t np, uint32_t flags, HistLayout &H) {
+  memset(&H, 0, sizeof H);
+  const bool waves = (flags & (GF_HIST_WAVES | GF_SORT_LOCALITY)) != 0;
+  if (!waves) {
+    H.total = 256;
+    return;
+  }
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  H.state = take(8 * np);
+  H.Ep = take(8 * np);
+  H.matp = take(np);
+  H.fb = take(np);
+  plan_batch(g, np, flags & GF_SORT_LOCALITY, true, true, H.B);
+  H.slot = take(H.B.slot.bytes);
+  H.total = o;
+}
+
+gf_status gf_xs_history_bytes(const gf_xs_grid *g, uint64_t n_particles, uint32_t flags, size_t *scratch_bytes) {
+  if (!g || !scratch_bytes) return fail(GF_E_INVAL, "grid or scratch_bytes is NULL");
+  HistLayout H;
+  plan_history(g, n_particles, flags, H);
+  *scratch_bytes = H.total;
+  return GF_OK;
+}
+
+gf_status gf_xs_history_batch(const gf_xs_grid *g, uint64_t first_particle, uint64_t n_particles,
+                              int32_t lookups_per_particle, uint64_t starting_seed, uint32_t flags,
+                              double *d_macro_out, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                              gf_stream_t stream) {
+  try {
+    if (!g) return fail(GF_E_INVAL, "grid is NULL");
+    if (!d_vsum) return fail(GF_E_INVAL, "vsum is NULL");
+    if (flags & ~(uint32_t)(GF_SORT_LOCALITY | GF_HIST_WAVES)) return fail(GF_E_INVAL, "unknown flags 0x%x", flags);
+    const int L = lookups_per_particle;
+    if (L < 1 || L > (1 << 20)) return fail(GF_E_INVAL, "lookups_per_particle = %d outside [1, 2^20]", L);
+    if (n_particles >= (1ull << 32)) return fail(GF_E_INVAL, "n_particles >= 2^32: split the job");
+    HistLayout H;
+    plan_history(g, n_particles, flags, H);
+    if (n_particles && (!scratch || scratch_bytes < H.total))
+      return fail(GF_E_NOMEM, "scratch %zu B < required %zu B", scratch_bytes, H.total);
+    if (n_particles && ((uintptr_t)scratch & 255)) return fail(GF_E_INVAL, "scratch must be 256-byte aligned");
+    if (n_particles == 0) return GF_OK;
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return fail(GF_E_CUDA, "cannot make device %d current", g->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long *dvsum = reinterpret_cast<unsigned long long *>(d_vsum);
+    const uint32_t np = (uint32_t)n_particles;
+    const bool xs = g->p.bench == GF_XSBENCH;
+    const int ch = xs ? 5 : 4;
+    cudaError_t ce;
+    if (!(flags & (GF_HIST_WAVES | GF_SORT_LOCALITY))) {
+      ce = xs ? launch_xs_history_direct(g->xs, first_particle, np, L, starting_seed, d_macro_out, dvsum, st)
+              : launch_rs_history_direct(g->rs, first_particle, np, L, starting_seed, d_macro_out, dvsum, st);
+      if (ce != cudaSuccess) return fail(GF_E_CUDA, "history launch: %s", cudaGetErrorString(ce));
+      return GF_OK;
+    }
+    char *sc = static_cast<char *>(scratch);
+    uint64_t *state = reinterpret_cast<uint64_t *>(sc + H.state);
+    double *Ep = reinterpret_cast<double *>(sc + H.Ep);
+    uint8_t *matp = reinterpret_cast<uint8_t *>(sc + H.matp);
+    uint8_t *fb = reinterpret_cast<uint8_t *>(sc + H.fb);
+    const SortScratch S = slot_sort(sc + H.slot, H.B.slot);
+    const bool sort = (flags & GF_SORT_LOCALITY) != 0;
+    const uint64_t stride = (uint64_t)L * (xs ? 8ull : 2ull);
+    const double *thr = xs ? g->xs.thr : g->rs.thr;
+    for (int i = 0; i < L; i++) {
+      ce = launch_hist_sample(g->p.bench, first_particle, np, starting_seed, stride, i, thr, state, fb, Ep, matp, st);
+      if (ce != cudaSuccess) return fail(GF_E_CUDA, "history sample launch: %s", cudaGetErrorString(ce));
+      // the last wave's feedback is never read
+      OutSpec out{d_macro_out ? d_macro_out + (size_t)i * ch : nullptr, (uint32_t)(L * ch), i + 1 < L ? fb : nullptr,
+                  xs ? 1.0 : 0.0};
+      ce = xs ? launch_xs_lookup(g->xs, 0, np, 0, Ep, matp, sort, S, out, dvsum, st)
+              : launch_rs_lookup(g->rs, 0, np, 0, Ep, matp, sort, S, out, dvsum, st);
+      if (ce != cudaSuccess) return fail(GF_E_CUDA, "history wave launch: %s", cudaGetErrorString(ce));
+    }
+    return GF_OK;
   } catch (...) {
     return fail(GF_E_NOMEM, "host allocation failed");
   }

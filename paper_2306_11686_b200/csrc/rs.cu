@@ -254,7 +254,7 @@ constexpr int kRsTpb = 128;
 __global__ void __launch_bounds__(kRsTpb) rs_lookup_direct(RsDev R, uint64_t first, uint32_t n, uint64_t seed,
                                                            const double *__restrict__ src_E,
                                                            const uint8_t *__restrict__ src_mat,
-                                                           double *__restrict__ macro_out,
+                                                           OutSpec out,
                                                            unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Tables T = stage_tables(R.total, R.moff, R.mnuc, R.mconc, R.thr, smem);
@@ -275,10 +275,7 @@ __global__ void __launch_bounds__(kRsTpb) rs_lookup_direct(RsDev R, uint64_t fir
     double m[4];
     rs_macro(R, T, E, mat, m);
     v = argmax4_plus1(m);
-    if (macro_out) {
-#pragma unroll
-      for (int c = 0; c < 4; c++) macro_out[(size_t)t * 4 + c] = m[c];
-    }
+    if (out.any()) write_out<4>(out, t, m);
   }
   hash_epilogue(v, vsum);
 }
@@ -286,7 +283,7 @@ __global__ void __launch_bounds__(kRsTpb) rs_lookup_direct(RsDev R, uint64_t fir
 __global__ void __launch_bounds__(kRsTpb) rs_lookup_sorted(RsDev R, uint32_t n, const double *__restrict__ Es,
                                                            const uint32_t *__restrict__ idx,
                                                            const uint32_t *__restrict__ mstart,
-                                                           double *__restrict__ macro_out,
+                                                           OutSpec out,
                                                            unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Tables T = stage_tables(R.total, R.moff, R.mnuc, R.mconc, R.thr, smem);
@@ -300,28 +297,62 @@ __global__ void __launch_bounds__(kRsTpb) rs_lookup_sorted(RsDev R, uint32_t n, 
     double m[4];
     rs_macro(R, T, Es[p], mat, m);
     v = argmax4_plus1(m);
-    if (macro_out) {
-      const size_t o = (size_t)idx[p] * 4;
+    if (out.any()) write_out<4>(out, idx[p], m);
+  }
+  hash_epilogue(v, vsum);
+}
+
+// History-based mode, direct mapping (history.cu; R-HIST-RS): one thread per particle, L dependent
+// lookups; start at fast_forward(seed, 2 L p); after each lookup add 1337 p (macro_c > 0) or 42 per
+// channel to the stream state (u64), then draw E and the material.  macro: NULL or [np][L][4].
+__global__ void __launch_bounds__(kRsTpb) rs_history_direct(RsDev R, uint64_t first_p, uint32_t np, int L,
+                                                            uint64_t seed, double *__restrict__ macro,
+                                                            unsigned long long *__restrict__ vsum) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Tables T = stage_tables(R.total, R.moff, R.mnuc, R.mconc, R.thr, smem);
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = 0;
+  if (t < np) {
+    const uint64_t p = first_p + t;
+    uint64_t s = lcg_skip(seed, p * (uint64_t)L * 2ull);
+    double E = lcg_draw(s);
+    int mat = pick_material(lcg_draw(s), T.thr);
+    for (int i = 0; i < L; i++) {
+      double m[4];
+      rs_macro(R, T, E, mat, m);
+      v += argmax4_plus1(m);
+      if (macro) {
 #pragma unroll
-      for (int c = 0; c < 4; c++) macro_out[o + c] = m[c];
+        for (int c = 0; c < 4; c++) macro[((size_t)t * L + i) * 4 + c] = m[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 4; c++) s += m[c] > 0.0 ? 1337ull * p : 42ull;
+      E = lcg_draw(s);
+      mat = pick_material(lcg_draw(s), T.thr);
     }
   }
   hash_epilogue(v, vsum);
 }
 
+cudaError_t launch_rs_history_direct(const RsDev &R, uint64_t first_p, uint32_t np, int L, uint64_t seed,
+                                     double *macro, unsigned long long *vsum, cudaStream_t st) {
+  rs_history_direct<<<nblk(np, kRsTpb), kRsTpb, table_smem(R.total), st>>>(R, first_p, np, L, seed, macro, vsum);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rs_lookup(const RsDev &R, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
-                             const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
+                             const uint8_t *src_mat, bool sort, const SortScratch &S, const OutSpec &out,
                              unsigned long long *vsum, cudaStream_t st, cudaEvent_t ev_mid) {
   const size_t smem = table_smem(R.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, R.thr, S, macro_out != nullptr, st)) != cudaSuccess)
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, R.thr, S, out.any(), st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    rs_lookup_sorted<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, n, S.Es, S.idx, S.mstart, macro_out, vsum);
+    rs_lookup_sorted<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, n, S.Es, S.idx, S.mstart, out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    rs_lookup_direct<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, first, n, seed, src_E, src_mat, macro_out, vsum);
+    rs_lookup_direct<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, first, n, seed, src_E, src_mat, out, vsum);
   }
   return cudaGetLastError();
 }

@@ -327,7 +327,7 @@ template <int GT>
 __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t first, uint32_t n, uint64_t seed,
                                                                const double *__restrict__ src_E,
                                                                const uint8_t *__restrict__ src_mat,
-                                                               double *__restrict__ macro_out,
+                                                               OutSpec out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
@@ -348,10 +348,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
     double m[5];
     macro_xs<GT, false>(X, T, E, energy_index<GT>(X, E), mat, m);
     v = argmax5_plus1(m);
-    if (macro_out) {
-#pragma unroll
-      for (int c = 0; c < 5; c++) macro_out[(size_t)t * 5 + c] = m[c];
-    }
+    if (out.any()) write_out<5>(out, t, m);
   }
   hash_epilogue(v, vsum);
 }
@@ -362,7 +359,7 @@ template <int GT>
 __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t n, const double *__restrict__ Es,
                                                                const uint32_t *__restrict__ idx,
                                                                const uint32_t *__restrict__ mstart,
-                                                               double *__restrict__ macro_out,
+                                                               OutSpec out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
@@ -377,11 +374,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
     double m[5];
     macro_xs<GT, GT == GF_GRID_UNIONIZED>(X, T, E, energy_index<GT>(X, E), mat, m);
     v = argmax5_plus1(m);
-    if (macro_out) {
-      const size_t o = (size_t)idx[p] * 5;
-#pragma unroll
-      for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
-    }
+    if (out.any()) write_out<5>(out, idx[p], m);
   }
   hash_epilogue(v, vsum);
 }
@@ -412,45 +405,98 @@ static int sorted_kernel() {
 
 template <int GT>
 static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
-                             const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
+                             const uint8_t *src_mat, bool sort, const SortScratch &S, const OutSpec &out,
                              unsigned long long *vsum, cudaStream_t st, cudaEvent_t ev_mid) {
   const size_t smem = xs_table_smem(X.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, macro_out != nullptr, st)) != cudaSuccess)
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
     if (GT == GF_GRID_UNIONIZED && sorted_kernel() == kKernStaged)
-      return X.fastdiv ? launch_staged<true>(X, n, S, macro_out, vsum, st)
-                       : launch_staged<false>(X, n, S, macro_out, vsum, st);
+      return X.fastdiv ? launch_staged<true>(X, n, S, out, vsum, st)
+                       : launch_staged<false>(X, n, S, out, vsum, st);
     if (GT != GF_GRID_NUCLIDE && sorted_kernel() != kKernThread)
-      return X.fastdiv ? launch_group<GT, true>(X, n, S, macro_out, vsum, st)
-                       : launch_group<GT, false>(X, n, S, macro_out, vsum, st);
+      return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
+                       : launch_group<GT, false>(X, n, S, out, vsum, st);
     if (GT == GF_GRID_NUCLIDE && sorted_kernel() != kKernThread) {
-      xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out,
+      xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                            vsum);
       return cudaGetLastError();
     }
-    xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, macro_out, vsum);
+    xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    xs_lookup_direct<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, first, n, seed, src_E, src_mat, macro_out,
+    xs_lookup_direct<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, first, n, seed, src_E, src_mat, out,
                                                                         vsum);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_xs_lookup(const XsDev &X, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
-                             const uint8_t *src_mat, bool sort, const SortScratch &S, double *macro_out,
+                             const uint8_t *src_mat, bool sort, const SortScratch &S, const OutSpec &out,
                              unsigned long long *vsum, cudaStream_t st, cudaEvent_t ev_mid) {
   switch (X.grid_type) {
     case GF_GRID_NUCLIDE:
-      return launch_gt<GF_GRID_NUCLIDE>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+      return launch_gt<GF_GRID_NUCLIDE>(X, first, n, seed, src_E, src_mat, sort, S, out, vsum, st, ev_mid);
     case GF_GRID_UNIONIZED:
-      return launch_gt<GF_GRID_UNIONIZED>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+      return launch_gt<GF_GRID_UNIONIZED>(X, first, n, seed, src_E, src_mat, sort, S, out, vsum, st, ev_mid);
     default:
-      return launch_gt<GF_GRID_HASH>(X, first, n, seed, src_E, src_mat, sort, S, macro_out, vsum, st, ev_mid);
+      return launch_gt<GF_GRID_HASH>(X, first, n, seed, src_E, src_mat, sort, S, out, vsum, st, ev_mid);
   }
+}
+
+// ------------------------------------------------------------------------------------------ NEXT-1
+// History-based mode, direct mapping (history.cu): one thread per particle runs its L dependent
+// lookups (R-HIST): start at fast_forward(seed, 8 L p); after each lookup skip #{c : macro_c > 1.0}
+// draws, then draw E and the material.  macro: NULL or [np][L][5].
+template <int GT>
+__global__ void __launch_bounds__(kLookupTpb) xs_history_direct(XsDev X, uint64_t first_p, uint32_t np, int L,
+                                                                uint64_t seed, double *__restrict__ macro,
+                                                                unsigned long long *__restrict__ vsum) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const XsTables T = stage_xs_tables(X, smem);
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = 0;
+  if (t < np) {
+    const uint64_t p = first_p + t;
+    uint64_t s = lcg_skip(seed, p * (uint64_t)L * 8ull);
+    double E = lcg_draw(s);
+    int mat = pick_material(lcg_draw(s), T.thr);
+    for (int i = 0; i < L; i++) {
+      double m[5];
+      macro_xs<GT, false>(X, T, E, energy_index<GT>(X, E), mat, m);
+      v += argmax5_plus1(m);
+      if (macro) {
+#pragma unroll
+        for (int c = 0; c < 5; c++) macro[((size_t)t * L + i) * 5 + c] = m[c];
+      }
+      uint32_t nf = 0;
+#pragma unroll
+      for (int c = 0; c < 5; c++) nf += m[c] > 1.0 ? 1u : 0u;
+      for (uint32_t k = 0; k < nf; k++) s = lcg_next(s);
+      E = lcg_draw(s);
+      mat = pick_material(lcg_draw(s), T.thr);
+    }
+  }
+  hash_epilogue(v, vsum);
+}
+
+cudaError_t launch_xs_history_direct(const XsDev &X, uint64_t first_p, uint32_t np, int L, uint64_t seed,
+                                     double *macro, unsigned long long *vsum, cudaStream_t st) {
+  const size_t smem = xs_table_smem(X.total);
+  const unsigned g = nblk(np, kLookupTpb);
+  switch (X.grid_type) {
+    case GF_GRID_NUCLIDE:
+      xs_history_direct<GF_GRID_NUCLIDE><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
+      break;
+    case GF_GRID_UNIONIZED:
+      xs_history_direct<GF_GRID_UNIONIZED><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
+      break;
+    default:
+      xs_history_direct<GF_GRID_HASH><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
+  }
+  return cudaGetLastError();
 }
 
 // Self-test hook for the exact reciprocal division (tests): out[i] = div_rn(a[i], b[i], RN(1/b[i]))

@@ -166,7 +166,7 @@ template <int GT, bool FAST>
 __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
     xs_lookup_group(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
                     const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart,
-                    double *__restrict__ macro_out, unsigned long long *__restrict__ vsum) {
+                    OutSpec out, unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t ms[kMats + 1];  // material segment starts (SMEM: registers go to the loop)
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
@@ -225,18 +225,14 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
     }
     for (uint32_t i = 0; i < nl; i++) {
       vacc += argmax5_plus1(m[i]);
-      if (macro_out) {
-        const size_t o = (size_t)idx[p0 + i] * 5;
-#pragma unroll
-        for (int c = 0; c < 5; c++) macro_out[o + c] = m[i][c];
-      }
+      if (out.any()) write_out<5>(out, idx[p0 + i], m[i]);
     }
   }
   hash_epilogue(vacc, vsum);
 }
 
 template <int GT, bool FAST>
-static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S, double *macro_out,
+static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
                                 unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = xs_table_smem(X.total);
   static int blocks_per_sm = 0;
@@ -255,6 +251,6 @@ static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S
   const uint32_t grid = min((ngroups + kTpbL - 1) / kTpbL, (uint32_t)(sms * max(blocks_per_sm, 1)));
   idx_prep<GT><<<nblk(n, 256), 256, 0, st>>>(X, n, S.Es, S.us);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, macro_out, vsum);
+  xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum);
   return cudaGetLastError();
 }

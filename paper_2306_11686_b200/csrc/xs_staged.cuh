@@ -179,7 +179,7 @@ template <bool FAST>
 __global__ void __launch_bounds__(kStagedThreads, 3)
     xs_lookup_staged(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ us,
                      const TileInfo *__restrict__ tinfo, const uint32_t *__restrict__ idx,
-                     const uint32_t *__restrict__ mstart, double *__restrict__ macro_out,
+                     const uint32_t *__restrict__ mstart, OutSpec out,
                      unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
@@ -252,18 +252,14 @@ __global__ void __launch_bounds__(kStagedThreads, 3)
     }
     if (p < n) {
       vacc += argmax5_plus1(m);
-      if (macro_out) {
-        const size_t o = (size_t)idx[p] * 5;
-#pragma unroll
-        for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
-      }
+      if (out.any()) write_out<5>(out, idx[p], m);
     }
   }
   hash_epilogue(vacc, vsum);
 }
 
 template <bool FAST>
-static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &S, double *macro_out,
+static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
                                  unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = staged_smem(X.total);
   static int blocks_per_sm[2] = {0, 0};
@@ -286,7 +282,7 @@ static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &
   staged_prep<<<ntiles, kTile, 0, st>>>(X, n, S.Es, S.mstart, S.us, tinfo);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm[FAST], 1)));
-  xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.us, tinfo, S.idx, S.mstart, macro_out,
+  xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.us, tinfo, S.idx, S.mstart, out,
                                                              vsum);
   return cudaGetLastError();
 }

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_warp_nuclide(XsDev X, ui
                                                                      const double *__restrict__ Es,
                                                                      const uint32_t *__restrict__ idx,
                                                                      const uint32_t *__restrict__ mstart,
-                                                                     double *__restrict__ macro_out,
+                                                                     OutSpec out,
                                                                      unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
@@ -127,11 +127,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_warp_nuclide(XsDev X, ui
     }
     if (act) {
       v = argmax5_plus1(m);
-      if (macro_out) {
-        const size_t o = (size_t)idx[p] * 5;
-#pragma unroll
-        for (int c = 0; c < 5; c++) macro_out[o + c] = m[c];
-      }
+      if (out.any()) write_out<5>(out, idx[p], m);
     }
   }
   hash_epilogue(v, vsum);

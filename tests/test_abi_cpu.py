@@ -167,3 +167,11 @@ def test_shard_range_exact_cover():
                 nxt = lo + cnt
                 seen += cnt
             assert seen == n and nxt == n
+
+
+def test_history_argument_checks():
+    """gf_xs_history_batch validates synchronously, before any CUDA call (no GPU here)."""
+    L = gf.lib()
+    assert L.gf_xs_history_batch(None, 0, 10, 34, 1070, 0, None, None, None, 0, None) == 1
+    b = C.c_size_t()
+    assert L.gf_xs_history_bytes(None, 10, 0, C.byref(b)) == 1

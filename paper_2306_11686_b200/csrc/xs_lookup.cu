@@ -386,21 +386,24 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 #include "xs_sorted_u.cuh"
 #include "xs_warp_nuclide.cuh"
 
-// Kernel for the sorted path.  GF_XS_KERNEL in the environment selects an alternative for A/B
-// measurements: "staged" (TMA producer/consumer ring, unionized only), "thread" (non-persistent,
-// one lookup per thread, per-lane bisection on the nuclide grid); default "group" (persistent, kL
-// lookups per thread; unionized and hash grids) and, on the nuclide grid, the warp-cooperative
-// search kernel.  All give identical results.
+// Kernel for the sorted path.  Default: the persistent group kernel (kL lookups per thread sharing
+// record loads) for dense batches, n >= kGroupMinN, and the one-lookup-per-thread kernel below it:
+// a sparse batch (a history wave, a host-IO chunk) has few lookups per interval, so record sharing
+// buys little while the group kernel's 4x fewer threads leave the DRAM latency exposed (measured,
+// DESIGN.md Sec. 7).  The nuclide grid uses the warp-cooperative search kernel.  GF_XS_KERNEL in the
+// environment forces an alternative for A/B measurements ("group", "thread", "staged" = the TMA
+// producer/consumer ring, unionized only); GF_XS_GROUP_MIN overrides the threshold.  All give
+// identical results.  (Read on every launch: the tests and A/B tools switch it within a process.)
 enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2 };
-static int sorted_kernel() {
-  static int v = -1;
-  if (v < 0) {
-    const char *s = getenv("GF_XS_KERNEL");
-    v = kKernGroup;
-    if (s && s[0] == 's') v = kKernStaged;
-    if (s && s[0] == 't') v = kKernThread;
-  }
-  return v;
+constexpr uint32_t kGroupMinN = 6u << 20;  // crossover measured at 4-8 M (tools/ab_batch_n.py)
+static int sorted_kernel(uint32_t n) {
+  const char *s = getenv("GF_XS_KERNEL");
+  if (s && s[0] == 's') return kKernStaged;
+  if (s && s[0] == 't') return kKernThread;
+  if (s && s[0] == 'g') return kKernGroup;
+  const char *m = getenv("GF_XS_GROUP_MIN");
+  const uint32_t nmin = m ? (uint32_t)strtoul(m, nullptr, 10) : kGroupMinN;
+  return n >= nmin ? kKernGroup : kKernThread;
 }
 
 template <int GT>
@@ -413,13 +416,15 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    if (GT == GF_GRID_UNIONIZED && sorted_kernel() == kKernStaged)
+    const int kern = sorted_kernel(n);
+    if (GT == GF_GRID_UNIONIZED && kern == kKernStaged)
       return X.fastdiv ? launch_staged<true>(X, n, S, out, vsum, st)
                        : launch_staged<false>(X, n, S, out, vsum, st);
-    if (GT != GF_GRID_NUCLIDE && sorted_kernel() != kKernThread)
+    if (GT != GF_GRID_NUCLIDE && kern == kKernGroup)
       return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
                        : launch_group<GT, false>(X, n, S, out, vsum, st);
-    if (GT == GF_GRID_NUCLIDE && sorted_kernel() != kKernThread) {
+    const char *force = getenv("GF_XS_KERNEL");
+    if (GT == GF_GRID_NUCLIDE && !(force && force[0] == 't')) {
       xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                            vsum);
       return cudaGetLastError();

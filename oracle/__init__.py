@@ -80,6 +80,7 @@ def lib():
         L.rso_macro.restype = None; L.rso_macro.argtypes = [vp, dbl, i32, vp, P(dbl)]
         L.rso_lookup_batch.restype = u64; L.rso_lookup_batch.argtypes = [vp, u64, u64, u64, vp, vp, i32]
         L.rso_lookup_indices.restype = u64; L.rso_lookup_indices.argtypes = [vp, vp, u64, u64, vp, vp]
+        L.rso_set_doppler.restype = None; L.rso_set_doppler.argtypes = [vp, i32]
         L.xso_history_batch.restype = u64; L.xso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, i32]
         L.rso_history_batch.restype = u64; L.rso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, vp, i32]
         _lib = L
@@ -257,11 +258,12 @@ class XSOracle:
 
 # ------------------------------------------------------------------ RSBench oracle
 class RSOracle:
-    def __init__(self, n_nuc=355, avg_poles=1000, avg_windows=100, numL=4, seed=GRID_SEED):
+    def __init__(self, n_nuc=355, avg_poles=1000, avg_windows=100, numL=4, seed=GRID_SEED, doppler=1):
         h = lib().rso_create(n_nuc, avg_poles, avg_windows, numL, seed)
         if not h:
             raise ValueError("rso_create rejected the parameters")
-        self.h, self.n_nuc, self.numL = h, n_nuc, numL
+        self.h, self.n_nuc, self.numL, self.doppler = h, n_nuc, numL, doppler
+        lib().rso_set_doppler(h, doppler)
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -540,7 +540,11 @@ typedef struct {
     double *win;               /* [total_windows][3]: T A F */
     int *win_start, *win_end;  /* [total_windows]; end is inclusive as generated (R-RSEND) */
     double *K0RS;              /* [n_nuc][numL] */
+    int doppler;               /* 1 (default): Doppler-broadened poles via W(z); 0: the 0 K kernel (R-RS0) */
 } rs_oracle;
+
+/* NEXT-3: select the 0 K (doppler = 0) or Doppler-broadened (doppler = 1) pole kernel. */
+void rso_set_doppler(rs_oracle *o, int doppler) { o->doppler = doppler ? 1 : 0; }
 
 /* RS data, one stream from `seed`, consumed in this order (SURVEY.md:594-603, R-RSGEN). */
 rs_oracle *rso_create(int n_nuc, int avg_poles, int avg_windows, int numL, uint64_t seed) {
@@ -613,6 +617,7 @@ rs_oracle *rso_create(int n_nuc, int avg_poles, int avg_windows, int numL, uint6
     o->K0RS = (double *)malloc(sizeof(double) * n_nuc * numL);
     for (int i = 0; i < n_nuc; i++)
         for (int l = 0; l < numL; l++) o->K0RS[i * numL + l] = o_lcg_double(&s);
+    o->doppler = 1;
     return o;
 }
 
@@ -643,7 +648,7 @@ void rso_data(const rs_oracle *o, double *pole, int *pole_l, double *win, int *w
 }
 
 /* B2-B3: micro xs (sigT, sigA, sigF, sigE) of nuclide `nuc` at E, Doppler-broadened
- * (SURVEY.md:609-617).  *scale receives sum of |terms| (the R-UNIQ cancellation scale). */
+ * (SURVEY.md:609-617), or at 0 K when o->doppler == 0 (NEXT-3, reading R-RS0).  *scale receives sum of |terms| (the R-UNIQ cancellation scale). */
 static void rso_micro(const rs_oracle *o, int nuc, double E, double micro[4], double *scale) {
     double spacing = 1.0 / o->n_windows[nuc];
     int w = (int)(E / spacing);
@@ -671,10 +676,16 @@ static void rso_micro(const rs_oracle *o, int nuc, double E, double micro[4], do
     for (int p = o->win_start[q]; p < o->win_end[q]; p++) { /* [start, end): R-RSEND */
         const double *P = o->pole + (o->pole_off[nuc] + p) * 8;
         o_cplx EA = {P[0], P[1]}, RT = {P[2], P[3]}, RA = {P[4], P[5]}, RF = {P[6], P[7]};
-        o_cplx Ec = {E, 0.0}, dopp = {0.5, 0.0};
-        o_cplx Z = c_mul(c_sub(Ec, EA), dopp);
         o_cplx W;
-        rso_fast_nuclear_W(Z.r, Z.i, &W.r, &W.i);
+        if (o->doppler) {
+            o_cplx Ec = {E, 0.0}, dopp = {0.5, 0.0};
+            o_cplx Z = c_mul(c_sub(Ec, EA), dopp);
+            rso_fast_nuclear_W(Z.r, Z.i, &W.r, &W.i);
+        } else { /* 0 K (R-RS0): PSIIKI = i / (EA - sqrt(E)); CDUM = PSIIKI / E; W := CDUM */
+            o_cplx t1 = {0.0, 1.0}, t2 = {sqrt(E), 0.0}, Ec = {E, 0.0};
+            o_cplx psiiki = c_div(t1, c_sub(EA, t2));
+            W = c_div(psiiki, Ec);
+        }
         double t = c_mul(RT, c_mul(W, fac[o->pole_l[o->pole_off[nuc] + p]])).r;
         double a = c_mul(RA, W).r;
         double f = c_mul(RF, W).r;

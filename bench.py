@@ -36,6 +36,7 @@ CONFIGS = {
     "C4": ("xs", 355, 2, 170_000_000, "XSBench large 355x11303, hash grid 10000 bins, 170M event lookups"),
     "C5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, windowed multipole + Faddeeva, 10.2M lookups"),
     # NEXT-3: the nuclide grid at scale -- not a BASELINE.json config
+    "C5D0": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, 0 K multipole kernel (doppler off, NEXT-3), 10.2M lookups"),
     "C3N": ("xs", 355, 0, 17_000_000, "XSBench large 355x11303, nuclide-grid search, 17M event lookups (NEXT-3)"),
     # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
     "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
@@ -46,9 +47,10 @@ HIST_L = {"H2": 34, "H3": 34, "H5": 34}  # lookups per particle (history configs
 # Per-lookup algorithmic work of the dominant kernel:
 #   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
 #   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
-#   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop).
+#   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop);
+#   C5D0 (0 K): 55.4 x (51 + 9.09 x 43 per pole: sqrt, two textbook complex divisions, 3 products) ~ 24,500.
 ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
-       "C3N": (0, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
+       "C3N": (0, 1551), "C5D0": (0, 24500), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
 
 
 def oracle_run(o, cfg, first, n, threads):
@@ -164,7 +166,7 @@ def cpu_baseline(cfg_name, seconds=12.0):
     if bench == "xs":
         o = O.XSOracle(n_iso, 11303, gt, bins=10000)
     else:
-        o = O.RSOracle(n_iso, 1000, 100, 4)
+        o = O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1)
     k = 20_000
     t = time.perf_counter()
     _, k = oracle_run(o, cfg_name, 0, k, threads)
@@ -186,7 +188,8 @@ def run_reference(args, rank, world):
     cfg_name = args.config
     bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
-    o = O.XSOracle(n_iso, 11303, gt, bins=10000) if bench == "xs" else O.RSOracle(n_iso, 1000, 100, 4)
+    o = (O.XSOracle(n_iso, 11303, gt, bins=10000) if bench == "xs"
+         else O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1))
     t = time.perf_counter()
     _, k0 = oracle_run(o, cfg_name, 0, 20_000, threads)
     per = (time.perf_counter() - t) / k0
@@ -269,7 +272,8 @@ def main():
     # ---------------------------------------------------------------- A0: grid build (untimed)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    params = gf.Params.xsbench(n_iso, 11303, gt, 10000) if bench == "xs" else gf.Params.rsbench(n_iso)
+    params = (gf.Params.xsbench(n_iso, 11303, gt, 10000) if bench == "xs"
+              else gf.Params.rsbench(n_iso, doppler=0 if args.config == "C5D0" else 1))
     grid = gf.Grid(params, device=dev)
     e1.record()
     torch.cuda.synchronize()

@@ -68,7 +68,9 @@ typedef struct {
     int32_t avg_n_poles;    /* RS: average poles per nuclide (1000); >= 1 */
     int32_t avg_n_windows;  /* RS: average windows per nuclide (100); >= 1 */
     int32_t numL;           /* RS: must be 4 */
-    int32_t doppler;        /* RS: must be 1 (Doppler-broadened kernel; 0 is NEXT-3, GF_E_UNSUPPORTED) */
+    int32_t doppler;        /* RS: 1 = Doppler-broadened poles through the Faddeeva function (default);
+                               0 = the 0 K kernel, sigma += Re(R i / ((EA - sqrt E) E) [fac_l])
+                               (NEXT-3, reading R-RS0); other values GF_E_INVAL */
     uint64_t init_seed;     /* grid / data generation LCG seed (42) */
     const int32_t *num_nucs;/* NULL = built-in Hoogenboom-Martin tables; else HOST int32[12] ...   */
     const int32_t *mats;    /* ... and HOST int32[12 * max_num_nucs] row-major nuclide ids        */

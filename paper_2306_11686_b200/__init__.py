@@ -55,10 +55,11 @@ class Params(C.Structure):
         return p
 
     @classmethod
-    def rsbench(cls, n_isotopes=355, avg_n_poles=1000, avg_n_windows=100, seed=42):
+    def rsbench(cls, n_isotopes=355, avg_n_poles=1000, avg_n_windows=100, seed=42, doppler=1):
         p = cls()
         _check(lib().gf_xs_default_params(RSBENCH, C.byref(p)))
         p.n_isotopes, p.avg_n_poles, p.avg_n_windows, p.init_seed = n_isotopes, avg_n_poles, avg_n_windows, seed
+        p.doppler = doppler
         return p
 
 

@@ -129,7 +129,7 @@ static gf_status validate(const gf_xs_params *p) {
       return fail(GF_E_UNSUPPORTED, "index grid larger than 2^32 entries");
   } else {
     if (p->numL != 4) return fail(GF_E_INVAL, "numL must be 4 (got %d)", p->numL);
-    if (p->doppler != 1) return fail(GF_E_UNSUPPORTED, "doppler = %d: only the Doppler kernel is built (0 is NEXT-3)", p->doppler);
+    if (p->doppler != 0 && p->doppler != 1) return fail(GF_E_INVAL, "doppler must be 0 or 1 (got %d)", p->doppler);
     if (p->avg_n_poles < 1 || p->avg_n_windows < 1) return fail(GF_E_INVAL, "avg_n_poles / avg_n_windows must be >= 1");
     if ((long long)p->avg_n_poles * p->n_isotopes >= (1ll << 28)) return fail(GF_E_UNSUPPORTED, "too many poles");
   }
@@ -356,6 +356,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       const size_t tp = (size_t)p->avg_n_poles * n, tw = (size_t)p->avg_n_windows * n;
       R.n_nuc = n;
       R.total = total;
+      R.doppler = p->doppler;
       double *pole = reinterpret_cast<double *>(base + L.pole);
       int32_t *pole_l = reinterpret_cast<int32_t *>(base + L.pole_l);
       double4 *win = reinterpret_cast<double4 *>(base + L.win);

@@ -221,8 +221,15 @@ __device__ __forceinline__ void rs_macro(const RsDev &R, const Tables &T, double
       const double2 *P = reinterpret_cast<const double2 *>(R.pole + (size_t)(pbase + p) * 8);
       const double2 EA = __ldg(P), RT = __ldg(P + 1), RA = __ldg(P + 2), RF = __ldg(P + 3);
       const int l = __ldg(R.pole_l + pbase + p);
-      cplx Z = {(E - EA.x) * 0.5, (0.0 - EA.y) * 0.5};
-      cplx fw = faddeeva(Z);
+      cplx fw;
+      if (R.doppler) {
+        const cplx Z = {(E - EA.x) * 0.5, (0.0 - EA.y) * 0.5};
+        fw = faddeeva(Z);
+      } else {  // 0 K (R-RS0): i / (EA - sqrt E) / E = (d.i + i d.r) / (|d|^2 E), d = EA - sqrt E
+        const double dr = EA.x - sqrtE, di = EA.y;
+        const double inv = 1.0 / ((dr * dr + di * di) * E);
+        fw = {di * inv, dr * inv};
+      }
       // fac[l] by selects (a dynamic index would put fac in local memory)
       const double fr = l == 0 ? fac[0].r : (l == 1 ? fac[1].r : (l == 2 ? fac[2].r : fac[3].r));
       const double fi = l == 0 ? fac[0].i : (l == 1 ? fac[1].i : (l == 2 ? fac[2].i : fac[3].i));

@@ -122,9 +122,10 @@ def test_invalid_rs_params():
     p = gf.Params.rsbench()
     p.numL = 3
     assert _bytes(p)[0] == 1
-    p = gf.Params.rsbench()
-    p.doppler = 0
-    assert _bytes(p)[0] == 4
+    p = gf.Params.rsbench(doppler=0)  # the 0 K kernel (NEXT-3) is built
+    assert _bytes(p)[0] == 0
+    p.doppler = 2
+    assert _bytes(p)[0] == 1
 
 
 def test_custom_tables_validation():

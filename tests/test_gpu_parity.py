@@ -473,3 +473,22 @@ def test_rs_energies_api(gf, torch):
         assert np.all(np.abs(m_g[t] - m) <= 1e-10 * max(S, 1e-300)), t
         raw_o += O.argmax4_plus1(m)
     assert raw_g == raw_o
+
+
+@pytest.mark.parametrize("n_iso", [68, 355])
+def test_rs_zero_kelvin(gf, torch, n_iso):
+    """NEXT-3: the 0 K pole kernel (doppler = 0, R-RS0): data identical to the Doppler grid's, macro xs
+    within 1e-10 S of the oracle (R-UNIQ), raw sums equal, event (sorted / unsorted) and history."""
+    o = O.RSOracle(n_iso, doppler=0)
+    g = gf.Grid(gf.Params.rsbench(n_iso, doppler=0))
+    n = 20_000 if n_iso == 355 else 50_000
+    raw_o, m_o, S = o.lookup_batch(3_000_000, n, want_macro=True)
+    for sort in (True, False):
+        raw_g, m_g = g.lookup_batch(3_000_000, n, sort=sort, want_macro=True)
+        assert raw_g == raw_o
+        assert (np.abs(m_g.cpu().numpy() - m_o) / S[:, None]).max() <= 1e-10
+    raw_h, m_h, S_h = o.history_batch(11, 200, 34, want_macro=True)
+    for mode in ("direct", "sorted"):
+        r, m = g.history_batch(11, 200, 34, mode=mode, want_macro=True)
+        assert r == raw_h
+        assert (np.abs(m.cpu().numpy() - m_h) / S_h[..., None]).max() <= 1e-10

@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(kRsTpb) rs_history_direct(RsDev R, uint64_t fi
 
 cudaError_t launch_rs_history_direct(const RsDev &R, uint64_t first_p, uint32_t np, int L, uint64_t seed,
                                      double *macro, unsigned long long *vsum, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = allow_smem(rs_history_direct, table_smem(R.total))) != cudaSuccess) return e;
   rs_history_direct<<<nblk(np, kRsTpb), kRsTpb, table_smem(R.total), st>>>(R, first_p, np, L, seed, macro, vsum);
   return cudaGetLastError();
 }
@@ -356,9 +358,11 @@ cudaError_t launch_rs_lookup(const RsDev &R, uint64_t first, uint32_t n, uint64_
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, R.thr, S, out.any(), st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
+    if ((e = allow_smem(rs_lookup_sorted, smem)) != cudaSuccess) return e;
     rs_lookup_sorted<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, n, S.Es, S.idx, S.mstart, out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
+    if ((e = allow_smem(rs_lookup_direct, smem)) != cudaSuccess) return e;
     rs_lookup_direct<<<nblk(n, kRsTpb), kRsTpb, smem, st>>>(R, first, n, seed, src_E, src_mat, out, vsum);
   }
   return cudaGetLastError();

@@ -193,23 +193,50 @@ struct XsTables {
   const double *conc;
   const uint2 *ent;  // {nuc * n_gp, nuc * pitch}
   const double *thr;
+  const uint4 *pk;   // {nuc * n_gp, nuc * pitch, conc (2 words)}: ent + conc in one 16-B LDS
 };
 
+// PK: the group kernel's packed layout, one 16-B entry {nuc * n_gp, nuc * pitch, conc} (ent and conc
+// stay unset); otherwise the separate ent / conc arrays.
+template <bool PK = false>
 __device__ __forceinline__ XsTables stage_xs_tables(const XsDev &X, unsigned char *smem) {
   int32_t *s_off = reinterpret_cast<int32_t *>(smem);          // 16 ints
   double *s_thr = reinterpret_cast<double *>(smem + 64);       // 12 doubles -> 160
   double *s_conc = reinterpret_cast<double *>(smem + 160);     // total doubles
   uint2 *s_ent = reinterpret_cast<uint2 *>(smem + 160 + 8 * (size_t)X.total);
+  uint4 *s_pk = reinterpret_cast<uint4 *>(smem + 160);         // PK: 16-B aligned (160 % 16 == 0)
   const uint32_t pitch = (uint32_t)(X.grid_type == GF_GRID_UNIONIZED ? X.ig_pitch : X.hg_pitch);
   for (int t = threadIdx.x; t < X.total; t += blockDim.x) {
     const uint32_t nuc = (uint32_t)X.mnuc[t];
-    s_conc[t] = X.mconc[t];
-    s_ent[t] = make_uint2(nuc * (uint32_t)X.n_gp, nuc * pitch);
+    const double c = X.mconc[t];
+    if (PK) {
+      const unsigned long long cb = (unsigned long long)__double_as_longlong(c);
+      s_pk[t] = make_uint4(nuc * (uint32_t)X.n_gp, nuc * pitch, (uint32_t)cb, (uint32_t)(cb >> 32));
+    } else {
+      s_conc[t] = c;
+      s_ent[t] = make_uint2(nuc * (uint32_t)X.n_gp, nuc * pitch);
+    }
   }
   if (threadIdx.x < kMats + 1) s_off[threadIdx.x] = X.moff[threadIdx.x];
   if (threadIdx.x < kMats) s_thr[threadIdx.x] = X.thr[threadIdx.x];
   __syncthreads();
-  return XsTables{s_off, s_conc, s_ent, s_thr};
+  if (PK) return XsTables{s_off, nullptr, nullptr, s_thr, s_pk};
+  return XsTables{s_off, s_conc, s_ent, s_thr, nullptr};
+}
+
+__device__ __forceinline__ uint2 tab_ent(const XsTables &T, int j, bool pk) {
+  if (pk) {
+    const uint4 v = T.pk[j];
+    return make_uint2(v.x, v.y);
+  }
+  return T.ent[j];
+}
+__device__ __forceinline__ double tab_conc(const XsTables &T, int j, bool pk) {
+  if (pk) {
+    const uint4 v = T.pk[j];
+    return __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z));
+  }
+  return T.conc[j];
 }
 
 __host__ __device__ inline size_t xs_table_smem(int total) { return 160 + 16 * (size_t)total; }
@@ -395,7 +422,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
 // producer/consumer ring, unionized only); GF_XS_GROUP_MIN overrides the threshold.  All give
 // identical results.  (Read on every launch: the tests and A/B tools switch it within a process.)
 enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2 };
-constexpr uint32_t kGroupMinN = 6u << 20;  // crossover measured at 4-8 M (tools/ab_batch_n.py)
+constexpr uint32_t kGroupMinN = 4u << 20;  // crossover measured at ~4 M (tools/ab_batch_n.py)
 static int sorted_kernel(uint32_t n) {
   const char *s = getenv("GF_XS_KERNEL");
   if (s && s[0] == 's') return kKernStaged;
@@ -425,13 +452,16 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
                        : launch_group<GT, false>(X, n, S, out, vsum, st);
     const char *force = getenv("GF_XS_KERNEL");
     if (GT == GF_GRID_NUCLIDE && !(force && force[0] == 't')) {
+      if ((e = allow_smem(xs_lookup_warp_nuclide, smem)) != cudaSuccess) return e;
       xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                            vsum);
       return cudaGetLastError();
     }
+    if ((e = allow_smem(xs_lookup_sorted<GT>, smem)) != cudaSuccess) return e;
     xs_lookup_sorted<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out, vsum);
   } else {
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
+    if ((e = allow_smem(xs_lookup_direct<GT>, smem)) != cudaSuccess) return e;
     xs_lookup_direct<GT><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, first, n, seed, src_E, src_mat, out,
                                                                         vsum);
   }
@@ -491,14 +521,18 @@ cudaError_t launch_xs_history_direct(const XsDev &X, uint64_t first_p, uint32_t 
                                      double *macro, unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = xs_table_smem(X.total);
   const unsigned g = nblk(np, kLookupTpb);
+  cudaError_t e;
   switch (X.grid_type) {
     case GF_GRID_NUCLIDE:
+      if ((e = allow_smem(xs_history_direct<GF_GRID_NUCLIDE>, smem)) != cudaSuccess) return e;
       xs_history_direct<GF_GRID_NUCLIDE><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
       break;
     case GF_GRID_UNIONIZED:
+      if ((e = allow_smem(xs_history_direct<GF_GRID_UNIONIZED>, smem)) != cudaSuccess) return e;
       xs_history_direct<GF_GRID_UNIONIZED><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
       break;
     default:
+      if ((e = allow_smem(xs_history_direct<GF_GRID_HASH>, smem)) != cudaSuccess) return e;
       xs_history_direct<GF_GRID_HASH><<<g, kLookupTpb, smem, st>>>(X, first_p, np, L, seed, macro, vsum);
   }
   return cudaGetLastError();

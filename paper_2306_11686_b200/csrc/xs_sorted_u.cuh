@@ -23,7 +23,7 @@
 #define GF_GROUP_L 4
 #endif
 #ifndef GF_GROUP_MINB
-#define GF_GROUP_MINB 3
+#define GF_GROUP_MINB 4
 #endif
 constexpr int kL = GF_GROUP_L;  // lookups per thread (A/B: -DGF_GROUP_L=2 -DGF_GROUP_MINB=5)
 constexpr int kTpbL = 128;
@@ -46,8 +46,28 @@ struct Rec {
   double y;  // fast division path only
 };
 
+#ifndef GF_PACKTAB
+#define GF_PACKTAB 1  // group loop: record base + concentration from one 16-B shared load
+#endif
+
+#ifndef GF_LD256
+#define GF_LD256 1
+#endif
+
+// 32-B vector load through the read-only path (sm_100: LDG.E.ENL2.256): one LSU request instead of two.
+__device__ __forceinline__ void ldg256(const double *p, double2 &a, double2 &b) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+
 template <bool FAST>
 __device__ __forceinline__ void load_rec(const XsDev &X, uint32_t r, Rec &R) {
+#if GF_LD256  // records are 128-B aligned: three 32-B loads + the 8-B reciprocal (4 requests, not 7)
+  const double *q = X.XR + (size_t)r * 16;
+  ldg256(q, R.v0, R.v1);
+  ldg256(q + 4, R.v2, R.v3);
+  ldg256(q + 8, R.v4, R.v5);
+  if (FAST) R.y = __ldg(q + 12);
+#else
   const double2 *p = reinterpret_cast<const double2 *>(X.XR) + (size_t)r * 8;
   R.v0 = __ldg(p + 0);
   R.v1 = __ldg(p + 1);
@@ -56,6 +76,7 @@ __device__ __forceinline__ void load_rec(const XsDev &X, uint32_t r, Rec &R) {
   R.v4 = __ldg(p + 4);
   R.v5 = __ldg(p + 5);
   if (FAST) R.y = __ldg(X.XR + (size_t)r * 16 + 12);
+#endif
 }
 
 // f = (hi.E - E) / (hi.E - lo.E); x_c = hi_c - f (hi_c - lo_c); m_c += x_c * conc -- the same RN
@@ -84,6 +105,10 @@ __device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_ba
     accumulate_rec<FAST>(P, E[i], conc, m[i]);
   }
 }
+
+#ifndef GF_ONEBUF
+#define GF_ONEBUF 1  // one record register buffer: 128 registers, 16 warps/SM (measured: C3 lookup 3.61 -> 2.98 ms)
+#endif
 
 #ifndef GF_SHORTCUT
 #define GF_SHORTCUT 1
@@ -135,29 +160,46 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
   uint32_t kq[4][kL];
 #pragma unroll
   for (int i = 0; i < 3; i++)
-    if (j0 + i < j1) load_k<GT>(X, T.ent[j0 + i], E, ix, kq[i]);
-  Rec A, B;
-  uint32_t kA = kq[0][0], kB = 0xFFFFFFFFu;
-  load_rec<FAST>(X, T.ent[j0].x + kA, A);
+    if (j0 + i < j1) load_k<GT>(X, tab_ent(T, j0 + i, GF_PACKTAB), E, ix, kq[i]);
+  Rec A;
+  uint32_t kA = kq[0][0];
+#if !GF_ONEBUF
+  Rec B;
+  uint32_t kB = 0xFFFFFFFFu;
+  load_rec<FAST>(X, tab_ent(T, j0, GF_PACKTAB).x + kA, A);
+#endif
   for (int j = j0; j < j1; j += 4) {
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const int jj = j + i;
       if (jj >= j1) break;
+#if GF_ONEBUF  // one record buffer, loaded at the top of the iteration (an L1 hit: prefetched 2 ahead)
+      Rec &cur = A;
+      uint32_t &kcur = kA;
+      kcur = kq[i][0];
+      const uint32_t rec_base = tab_ent(T, jj, GF_PACKTAB).x;  // (packed: one 16-B shared load for both)
+      const double conc = tab_conc(T, jj, GF_PACKTAB);
+      load_rec<FAST>(X, rec_base + kcur, cur);
+#else
       Rec &cur = (i & 1) ? B : A;
       Rec &nxt = (i & 1) ? A : B;
       uint32_t &kcur = (i & 1) ? kB : kA;
       uint32_t &knxt = (i & 1) ? kA : kB;
       if (jj + 1 < j1) {
         knxt = kq[(i + 1) & 3][0];
-        load_rec<FAST>(X, T.ent[jj + 1].x + knxt, nxt);
+        load_rec<FAST>(X, tab_ent(T, jj + 1, GF_PACKTAB).x + knxt, nxt);
       }
+#endif
       if (jj + kIgPf < j1)  // index-/hash-grid line of nuclide jj + kIgPf into L2 (no register cost)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(grid_line<GT>(X, T.ent[jj + kIgPf], ix[0])));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(grid_line<GT>(X, tab_ent(T, jj + kIgPf, GF_PACKTAB), ix[0])));
       if (jj + 2 < j1)  // the record of nuclide jj + 2 (its interval is in the ring) into L1
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(X.XR + (size_t)(T.ent[jj + 2].x + kq[(i + 2) & 3][0]) * 16));
-      if (jj + 3 < j1) load_k<GT>(X, T.ent[jj + 3], E, ix, kq[(i + 3) & 3]);
-      accumulate_group<FAST>(X, T.ent[jj].x, kq[i], cur, kcur, E, T.conc[jj], m);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(X.XR + (size_t)(tab_ent(T, jj + 2, GF_PACKTAB).x + kq[(i + 2) & 3][0]) * 16));
+      if (jj + 3 < j1) load_k<GT>(X, tab_ent(T, jj + 3, GF_PACKTAB), E, ix, kq[(i + 3) & 3]);
+#if GF_ONEBUF
+      accumulate_group<FAST>(X, rec_base, kq[i], cur, kcur, E, conc, m);
+#else
+      accumulate_group<FAST>(X, tab_ent(T, jj, GF_PACKTAB).x, kq[i], cur, kcur, E, tab_conc(T, jj, GF_PACKTAB), m);
+#endif
     }
   }
 }
@@ -170,7 +212,7 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t ms[kMats + 1];  // material segment starts (SMEM: registers go to the loop)
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
-  const XsTables T = stage_xs_tables(X, smem);  // (its __syncthreads also publishes ms)
+  const XsTables T = stage_xs_tables<GF_PACKTAB>(X, smem);  // (its __syncthreads also publishes ms)
   uint32_t vacc = 0;
   const uint32_t ngroups = (n + kL - 1) / kL;
   for (uint32_t g = blockIdx.x * kTpbL + threadIdx.x; g < ngroups; g += gridDim.x * kTpbL) {
@@ -210,13 +252,15 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
         const bool fi = FAST && fabs(E[i]) <= 2.0;
         for (int j = j0; j < j1; j++) {  // plain loop: these lookups are a handful per batch
           Rec P;
-          const uint32_t rec = T.ent[j].x + interval<GT>(X, T.ent[j], E[i], ix[i]);
+          const uint2 ej = tab_ent(T, j, GF_PACKTAB);
+          const uint32_t rec = ej.x + interval<GT>(X, ej, E[i], ix[i]);
+          const double cj = tab_conc(T, j, GF_PACKTAB);
           if (fi) {
             load_rec<FAST>(X, rec, P);
-            accumulate_rec<FAST>(P, E[i], T.conc[j], mi);
+            accumulate_rec<FAST>(P, E[i], cj, mi);
           } else {
             load_rec<false>(X, rec, P);
-            accumulate_rec<false>(P, E[i], T.conc[j], mi);
+            accumulate_rec<false>(P, E[i], cj, mi);
           }
         }
 #pragma unroll
@@ -239,6 +283,7 @@ static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S
   static size_t smem_cfg = 0;
   cudaError_t e;
   if (smem_cfg != smem) {
+    if ((e = allow_smem(xs_lookup_group<GT, FAST>, smem)) != cudaSuccess) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_group<GT, FAST>, kTpbL, smem)) !=
         cudaSuccess)
       return e;

@@ -492,3 +492,20 @@ def test_rs_zero_kelvin(gf, torch, n_iso):
         r, m = g.history_batch(11, 200, 34, mode=mode, want_macro=True)
         assert r == raw_h
         assert (np.abs(m.cpu().numpy() - m_h) / S_h[..., None]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("grid_type", [0, 1, 2])
+def test_large_custom_tables_need_big_smem(gf, grid_type):
+    """3,600 table entries: the SMEM-staged tables exceed the 48 KB default (opt-in path); history too."""
+    rng = np.random.default_rng(3)
+    n_iso = 355
+    nn = np.full(12, 300, dtype=np.int32)
+    mats = np.stack([rng.permutation(n_iso)[:300] for _ in range(12)]).astype(np.int32)
+    o = O.XSOracle(n_iso, 200, grid_type, bins=97, num_nucs=nn, mats=mats)
+    g = gf.Grid(gf.Params.xsbench(n_iso, 200, grid_type, 97), num_nucs=nn, mats=mats)
+    for sort in (True, False):
+        check_lookups(o, g, 777, 20_000, sort=sort)
+    raw_o, m_o = o.history_batch(5, 300, 6, want_macro=True)
+    for mode in ("direct", "sorted"):
+        raw_g, m_g = g.history_batch(5, 300, 6, mode=mode, want_macro=True)
+        assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o)

@@ -346,6 +346,13 @@ def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
     for b in list(rng.integers(1, 10000, 20)) + [1, 9999]:
         e = b * (1.0 / 10000)
         Es += [e, math.nextafter(e, 0), math.nextafter(e, 2), e, math.nextafter(math.nextafter(e, 0), 0)]
+    for b in list(rng.integers(1, 2 ** 17, 30)) + [1, 2 ** 17 - 1]:  # bin-summary bin edges
+        e = float(b) * 2.0 ** -17
+        Es += [e, math.nextafter(e, 0), math.nextafter(e, 2), e, math.nextafter(math.nextafter(e, 2), 2)]
+    for nuc in (3, 33):  # gridpoints and neighbours within 2^-32 of the bin position (ambiguous q)
+        for k in rng.integers(0, o.n_gp - 1, 10):
+            e = float(G[nuc, k, 0])
+            Es += [e + d * 2.0 ** -40 for d in (-3, -1, 0, 1, 3)]
     Es += list(0.3 + rng.random(20000) * 1e-3)  # dense: about 20 lookups per interval per nuclide
     E = np.clip(np.array(Es), 0.0, 1.0)
     for mat in (0, 4, 7):

@@ -1,0 +1,174 @@
+// sort.cu -- A1/A2: sampling and the locality sort on sm_100a.
+//
+// Lookups are ordered by the key (material, floor(E 2^17)) -- 12 x 2^17 bins, ~18-36 lookups per
+// bin at 17 M -- so that neighbouring lookups share intervals in the lookup kernels; order inside a
+// bin is arbitrary (results are order-independent: integer hash, outputs scattered back through idx).
+// Counting sort: sort_count (sample, one global atomic per lookup on its bin), a two-kernel scan,
+// sort_scatter (sample again, atomic cursor, store E and the lookup position).  Sampling is
+// index-addressed (lookup i draws from fast_forward(seed, 2i)): a thread skips once and steps
+// through kRun consecutive lookups; the material roll is decided on the integer LCG state
+// (pick_material_state, exact).  Measured alternative: a two-level sort (coarse
+// buckets per CTA run, then a per-bucket fine sort) moved fewer DRAM bytes but was not faster.
+#include "gf_internal.cuh"
+
+namespace gf {
+
+#ifndef GF_DIAG_SCATTER
+#define GF_DIAG_SCATTER 0
+#endif
+constexpr int kRun = 16;  // consecutive lookups per thread in the sampling kernels
+__global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
+                                                  const double *__restrict__ src_E,
+                                                  const uint8_t *__restrict__ src_mat,
+                                                  const double *__restrict__ thr, uint32_t *__restrict__ counts) {
+  __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
+  if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
+  __syncthreads();
+  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
+  if (t0 >= n) return;
+  uint64_t s = 0;
+  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
+  for (int r = 0; r < kRun; r++) {
+    uint64_t t = t0 + r;
+    if (t >= n) break;
+    double E;
+    int mat;
+    if (src_E) {
+      E = src_E[t];
+      mat = src_mat[t];
+      mat = mat < kMats ? mat : kMats - 1;
+    } else {
+      E = lcg_draw(s);
+      s = lcg_next(s);
+      mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
+    }
+    atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
+  }
+}
+
+// Block-exclusive scan of kScanBlk counts per CTA (coalesced); writes local offsets and the CTA total.
+__global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restrict__ counts,
+                                                       uint32_t *__restrict__ cursor, uint32_t *__restrict__ btot) {
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b = blockIdx.x * kScanBlk + tid;
+  const uint32_t c = counts[b];
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  cursor[b] = x - c + (wid > 0 ? wsum[wid - 1] : 0u);
+  if (tid == kScanBlk - 1) btot[blockIdx.x] = wsum[31];
+}
+
+// Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n).
+__global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ cursor, const uint32_t *__restrict__ btot,
+                                                     uint32_t *__restrict__ mstart) {
+  __shared__ uint32_t s_off;
+  constexpr int nblocks = kBins / kScanBlk;
+  if (threadIdx.x < 32) {
+    uint32_t acc = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) acc += btot[i];
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if (threadIdx.x == 0) s_off = acc;
+    if (blockIdx.x == nblocks - 1) {
+      uint32_t all = 0;
+      for (int i = threadIdx.x; i < nblocks; i += 32) all += btot[i];
+      all = __reduce_add_sync(0xffffffffu, all);
+      if (threadIdx.x == 0) mstart[kMats] = all;
+    }
+  }
+  __syncthreads();
+  const int b = blockIdx.x * kScanBlk + threadIdx.x;
+  const uint32_t v = cursor[b] + s_off;
+  cursor[b] = v;
+  if (b % kNB == 0) mstart[b / kNB] = v;
+}
+
+__global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
+                                                    const double *__restrict__ src_E,
+                                                    const uint8_t *__restrict__ src_mat,
+                                                    const double *__restrict__ thr, uint32_t *__restrict__ cursor,
+                                                    double *__restrict__ Es, uint32_t *__restrict__ idx) {
+  __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
+  if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
+  __syncthreads();
+  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
+  if (t0 >= n) return;
+  const int cnt = (int)min((uint64_t)kRun, n - t0);
+  uint64_t s = 0;
+  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
+  // three phases so that the kRun cursor atomics (each an L2 round trip) are in flight together
+  double E[kRun];
+  uint32_t pos[kRun];
+#pragma unroll
+  for (int r = 0; r < kRun; r++) {
+    if (r < cnt) {
+      const uint64_t t = t0 + r;
+      int mat;
+      if (src_E) {
+        E[r] = src_E[t];
+        mat = src_mat[t];
+        mat = mat < kMats ? mat : kMats - 1;
+      } else {
+        E[r] = lcg_draw(s);
+        s = lcg_next(s);
+        mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
+      }
+      pos[r] = (uint32_t)(mat * kNB + sort_bin(E[r]));
+    }
+  }
+#if GF_DIAG_SCATTER == 1  // diagnostic (wrong results): stores at a hash position, no atomics
+#pragma unroll
+  for (int r = 0; r < kRun; r++)
+    if (r < cnt) pos[r] = (uint32_t)(((t0 + r) * 2654435761ull) % n);
+#else
+#pragma unroll
+  for (int r = 0; r < kRun; r++)
+    if (r < cnt) pos[r] = atomicAdd(cursor + pos[r], 1u);
+#endif
+#pragma unroll
+  for (int r = 0; r < kRun; r++) {
+    if (r < cnt) {
+#if GF_DIAG_SCATTER == 2  // diagnostic (wrong results): atomics only, no stores
+      if (E[r] < -1.0)
+#endif
+      Es[pos[r]] = E[r];
+      if (idx) idx[pos[r]] = (uint32_t)(t0 + r);
+    }
+  }
+}
+
+static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
+                                 const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
+                                 cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * kBins, st)) != cudaSuccess) return e;
+  unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
+  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  scan_local<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  scan_add<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr);
+  return cudaGetLastError();
+}
+
+}  // namespace gf

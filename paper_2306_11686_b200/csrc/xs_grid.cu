@@ -23,11 +23,26 @@ __constant__ double c_dist[kMats] = {0.140, 0.052, 0.275, 0.134, 0.154, 0.064,
 
 // T[m] = dist[m] + dist[m-1] + ... + dist[1] in that order; T[0] = 0 (R-PICK: the order fixes bits).
 __global__ void thresholds_kernel(double *thr) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int m = 0; m < kMats; m++) {
-    double run = 0.0;
-    for (int j = m; j > 0; j--) run = __dadd_rn(run, c_dist[j]);
-    thr[m] = run;
+  if (threadIdx.x == 0) {
+    for (int m = 0; m < kMats; m++) {
+      double run = 0.0;
+      for (int j = m; j > 0; j--) run = __dadd_rn(run, c_dist[j]);
+      thr[m] = run;
+    }
+  }
+  __syncthreads();
+  // Integer form for the samplers: roll = RN(s) 2^-63 is non-decreasing in the LCG state s, so
+  // roll < T[m]  <=>  s < S[m] = min{s : RN(s) 2^-63 >= T[m]} -- found by bisection over s with the
+  // same conversion, stored as u64 in thr[kMats + m].
+  const int m = threadIdx.x;
+  if (m < kMats) {
+    unsigned long long lo = 0ull, hi = 1ull << 63;  // predicate false at lo? search min s with P(s)
+    const double T = thr[m];
+    while (lo < hi) {
+      const unsigned long long mid = lo + ((hi - lo) >> 1);
+      if (__dmul_rn(__ull2double_rn(mid), 0x1p-63) >= T) hi = mid; else lo = mid + 1;
+    }
+    reinterpret_cast<unsigned long long *>(thr)[kMats + m] = lo;
   }
 }
 

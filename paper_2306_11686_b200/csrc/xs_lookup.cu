@@ -25,140 +25,11 @@
 
 namespace gf {
 
-constexpr int kRun = 8;          // consecutive lookups per thread in the sampling kernels
 constexpr int kLookupTpb = 128;  // lookup CTA size
 constexpr int kPrefetch = 8;     // nuclides of index-grid L2 prefetch lookahead
 
-// ------------------------------------------------------------------------------------------ A1/A2
-__global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
-                                                  const double *__restrict__ src_E,
-                                                  const uint8_t *__restrict__ src_mat,
-                                                  const double *__restrict__ thr, uint32_t *__restrict__ counts) {
-  __shared__ double sT[kMats];
-  if (threadIdx.x < kMats) sT[threadIdx.x] = thr[threadIdx.x];
-  __syncthreads();
-  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
-  if (t0 >= n) return;
-  uint64_t s = 0;
-  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
-  for (int r = 0; r < kRun; r++) {
-    uint64_t t = t0 + r;
-    if (t >= n) break;
-    double E;
-    int mat;
-    if (src_E) {
-      E = src_E[t];
-      mat = src_mat[t];
-      mat = mat < kMats ? mat : kMats - 1;
-    } else {
-      E = lcg_draw(s);
-      mat = pick_material(lcg_draw(s), sT);
-    }
-    atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
-  }
-}
-
-// Block-exclusive scan of kScanBlk counts per CTA (coalesced); writes local offsets and the CTA total.
-__global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restrict__ counts,
-                                                       uint32_t *__restrict__ cursor, uint32_t *__restrict__ btot) {
-  __shared__ uint32_t wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int b = blockIdx.x * kScanBlk + tid;
-  const uint32_t c = counts[b];
-  uint32_t x = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t w = wsum[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    wsum[lane] = w;
-  }
-  __syncthreads();
-  cursor[b] = x - c + (wid > 0 ? wsum[wid - 1] : 0u);
-  if (tid == kScanBlk - 1) btot[blockIdx.x] = wsum[31];
-}
-
-// Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n).
-__global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ cursor, const uint32_t *__restrict__ btot,
-                                                     uint32_t *__restrict__ mstart) {
-  __shared__ uint32_t s_off;
-  constexpr int nblocks = kBins / kScanBlk;
-  if (threadIdx.x < 32) {
-    uint32_t acc = 0;
-    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) acc += btot[i];
-    acc = __reduce_add_sync(0xffffffffu, acc);
-    if (threadIdx.x == 0) s_off = acc;
-    if (blockIdx.x == nblocks - 1) {
-      uint32_t all = 0;
-      for (int i = threadIdx.x; i < nblocks; i += 32) all += btot[i];
-      all = __reduce_add_sync(0xffffffffu, all);
-      if (threadIdx.x == 0) mstart[kMats] = all;
-    }
-  }
-  __syncthreads();
-  const int b = blockIdx.x * kScanBlk + threadIdx.x;
-  const uint32_t v = cursor[b] + s_off;
-  cursor[b] = v;
-  if (b % kNB == 0) mstart[b / kNB] = v;
-}
-
-__global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
-                                                    const double *__restrict__ src_E,
-                                                    const uint8_t *__restrict__ src_mat,
-                                                    const double *__restrict__ thr, uint32_t *__restrict__ cursor,
-                                                    double *__restrict__ Es, uint32_t *__restrict__ idx) {
-  __shared__ double sT[kMats];
-  if (threadIdx.x < kMats) sT[threadIdx.x] = thr[threadIdx.x];
-  __syncthreads();
-  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
-  if (t0 >= n) return;
-  uint64_t s = 0;
-  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
-  for (int r = 0; r < kRun; r++) {
-    uint64_t t = t0 + r;
-    if (t >= n) break;
-    double E;
-    int mat;
-    if (src_E) {
-      E = src_E[t];
-      mat = src_mat[t];
-      mat = mat < kMats ? mat : kMats - 1;
-    } else {
-      E = lcg_draw(s);
-      mat = pick_material(lcg_draw(s), sT);
-    }
-    uint32_t pos = atomicAdd(cursor + mat * kNB + sort_bin(E), 1u);
-    Es[pos] = E;
-    if (idx) idx[pos] = (uint32_t)t;
-  }
-}
-
+// A1/A2 (sampling, locality sort): sort.cu.
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
-
-cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
-                                 const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
-                                 cudaStream_t st) {
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * kBins, st)) != cudaSuccess) return e;
-  unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
-  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_local<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_add<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr);
-  return cudaGetLastError();
-}
 
 // ------------------------------------------------------------------------------------------ A3
 // Per-lookup energy-grid index: u (unionized) or b (hash); unused for the nuclide grid.

@@ -516,3 +516,19 @@ def test_large_custom_tables_need_big_smem(gf, grid_type):
     for mode in ("direct", "sorted"):
         raw_g, m_g = g.history_batch(5, 300, 6, mode=mode, want_macro=True)
         assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o)
+
+
+def test_integer_material_thresholds(gf, torch):
+    """The samplers decide the material on the integer LCG state: roll = RN(s) 2^-63 < T[m] iff
+    s < S[m].  S[m] (stored after T in the thresholds block) must be the least s with
+    float(s) 2^-63 >= T[m] (Python's int -> float conversion rounds to nearest)."""
+    o, g = make_pair(gf, 68, 40, O.UNIONIZED, custom=True)
+    t, _ = g.array("thresholds")
+    off = t.data_ptr() - g.buf.data_ptr()
+    raw = g.buf[off:off + 24 * 8].cpu().numpy()
+    T = raw[:96].view(np.float64)
+    S = raw[96:].view(np.uint64)
+    assert np.array_equal(T, O.thresholds())
+    for m in range(1, 12):
+        s = int(S[m])
+        assert float(s) * 2.0 ** -63 >= T[m] and float(s - 1) * 2.0 ** -63 < T[m], m

@@ -115,6 +115,16 @@ __device__ __forceinline__ void accumulate_group(const XsDev &X, uint32_t rec_ba
   }
 }
 
+// Prefetches (measured): on the unionized grid both pay (C3 lookup 2.90 ms vs 3.46
+// without); on the hash grid they cost more than they hide (C4 46.7 vs 44.5 ms without), and
+// issuing them from the first lane of each run of equal lines only (shuffle + compare) is slower.
+#ifndef GF_PF_L1
+#define GF_PF_L1 1
+#endif
+#ifndef GF_PF_L2
+#define GF_PF_L2 1
+#endif
+
 #ifndef GF_ONEBUF
 #define GF_ONEBUF 1  // one record register buffer: 128 registers, 16 warps/SM (measured: C3 lookup 3.61 -> 2.98 ms)
 #endif
@@ -228,9 +238,10 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
         load_rec<FAST>(X, tab_ent(T, jj + 1, GF_PACKTAB).x + knxt, nxt);
       }
 #endif
-      if (jj + kIgPf < j1)  // index-/hash-grid line of nuclide jj + kIgPf into L2 (no register cost)
+      constexpr bool kPf = GT != GF_GRID_HASH;
+      if (kPf && GF_PF_L2 && jj + kIgPf < j1)  // index-grid line of nuclide jj + kIgPf into L2
         asm volatile("prefetch.global.L2 [%0];" ::"l"(grid_line<GT>(X, tab_ent(T, jj + kIgPf, GF_PACKTAB), ix[0])));
-      if (jj + 2 < j1)  // the record of nuclide jj + 2 (its interval is in the ring) into L1
+      if (kPf && GF_PF_L1 && jj + 2 < j1)  // the record of nuclide jj + 2 (its interval is in the ring) into L1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(X.XR + (size_t)(tab_ent(T, jj + 2, GF_PACKTAB).x + kq[(i + 2) & 3][0]) * 16));
       if (jj + 3 < j1) load_k<GT>(X, tab_ent(T, jj + 3, GF_PACKTAB), E, ix, kq[(i + 3) & 3]);
 #if GF_ONEBUF

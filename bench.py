@@ -38,6 +38,9 @@ CONFIGS = {
     # NEXT-3: the nuclide grid at scale -- not a BASELINE.json config
     "C5D0": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, 0 K multipole kernel (doppler off, NEXT-3), 10.2M lookups"),
     "C3N": ("xs", 355, 0, 17_000_000, "XSBench large 355x11303, nuclide-grid search, 17M event lookups (NEXT-3)"),
+    # NEXT-2 point counts: XSBench XL, 238,847 gridpoints per nuclide (the hash grid: the unionized
+    # grid's index grid would be 355 x 84.8 M entries)
+    "C6": ("xs", 355, 2, 17_000_000, "XSBench XL 355x238847, hash grid 10000 bins, 17M event lookups (NEXT-2)"),
     # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
     "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
     "H3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
@@ -50,7 +53,7 @@ HIST_L = {"H2": 34, "H3": 34, "H5": 34}  # lookups per particle (history configs
 #   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop);
 #   C5D0 (0 K): 55.4 x (51 + 9.09 x 43 per pole: sqrt, two textbook complex divisions, 3 products) ~ 24,500.
 ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
-       "C3N": (0, 1551), "C5D0": (0, 24500), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
+       "C3N": (0, 1551), "C5D0": (0, 24500), "C6": (6203, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
 
 
 def oracle_run(o, cfg, first, n, threads):
@@ -164,7 +167,7 @@ def cpu_baseline(cfg_name, seconds=12.0):
     bench, n_iso, gt, n, _ = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
     if bench == "xs":
-        o = O.XSOracle(n_iso, 11303, gt, bins=10000)
+        o = O.XSOracle(n_iso, 238847 if cfg_name == "C6" else 11303, gt, bins=10000)
     else:
         o = O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1)
     k = 20_000
@@ -188,7 +191,7 @@ def run_reference(args, rank, world):
     cfg_name = args.config
     bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
-    o = (O.XSOracle(n_iso, 11303, gt, bins=10000) if bench == "xs"
+    o = (O.XSOracle(n_iso, 238847 if cfg_name == "C6" else 11303, gt, bins=10000) if bench == "xs"
          else O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1))
     t = time.perf_counter()
     _, k0 = oracle_run(o, cfg_name, 0, 20_000, threads)
@@ -272,7 +275,8 @@ def main():
     # ---------------------------------------------------------------- A0: grid build (untimed)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    params = (gf.Params.xsbench(n_iso, 11303, gt, 10000) if bench == "xs"
+    n_gp = 238847 if args.config == "C6" else 11303
+    params = (gf.Params.xsbench(n_iso, n_gp, gt, 10000) if bench == "xs"
               else gf.Params.rsbench(n_iso, doppler=0 if args.config == "C5D0" else 1))
     grid = gf.Grid(params, device=dev)
     e1.record()

@@ -207,9 +207,11 @@ class Grid:
               "mat_offsets": torch.int32, "thresholds": torch.float64, "rs_poles": torch.float64,
               "rs_pole_l": torch.int32, "rs_windows": torch.float64, "rs_K0RS": torch.float64,
               "rs_pole_off": torch.int32, "rs_win_off": torch.int32}[name]
+        if name == "hash_grid" and nb.value == self.params.n_isotopes * pitch.value * 4:
+            dt = torch.int32  # u32 entries above 65536 gridpoints (XL / XXL)
         t = raw.view(dt)
-        if dt == torch.int16:  # u16 interval indices (< n_gp <= 16384): non-negative as int16
-            t = t.to(torch.int32)
+        if dt == torch.int16:  # u16 interval indices (< n_gp <= 65536): widen without sign extension
+            t = t.to(torch.int32) & 0xFFFF
         return t, pitch.value
 
     # ----------------------------------------------------------------- lookups

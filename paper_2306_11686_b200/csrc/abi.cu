@@ -118,14 +118,18 @@ static gf_status validate(const gf_xs_params *p) {
   if (p->n_isotopes < 1) return fail(GF_E_INVAL, "n_isotopes %d < 1", p->n_isotopes);
   if (p->bench == GF_XSBENCH) {
     if (p->n_gridpoints < 2) return fail(GF_E_INVAL, "n_gridpoints %lld < 2", (long long)p->n_gridpoints);
-    if (p->n_gridpoints > kMaxSortGp)
-      return fail(GF_E_UNSUPPORTED, "n_gridpoints %lld > %d (in-SMEM grid sort limit; XL grids are NEXT-2)",
-                  (long long)p->n_gridpoints, kMaxSortGp);
+    if (p->n_gridpoints > kMaxGp)
+      return fail(GF_E_UNSUPPORTED, "n_gridpoints %lld > %d", (long long)p->n_gridpoints, kMaxGp);
+    if (p->grid_type == GF_GRID_UNIONIZED && p->n_gridpoints > kMaxGp16)
+      return fail(GF_E_UNSUPPORTED, "unionized grid with n_gridpoints %lld > %d (u16 index grid; its %lld-entry "
+                  "index grid would not fit anyway): use the hash or nuclide grid", (long long)p->n_gridpoints,
+                  kMaxGp16, (long long)p->n_isotopes * p->n_isotopes * p->n_gridpoints);
     if (p->grid_type < 0 || p->grid_type > 2) return fail(GF_E_INVAL, "grid_type %d", p->grid_type);
     if (p->grid_type == GF_GRID_HASH && p->hash_bins < 1) return fail(GF_E_INVAL, "hash_bins %d < 1", p->hash_bins);
     if ((long long)p->n_isotopes * p->n_gridpoints >= (1ll << 31))
       return fail(GF_E_UNSUPPORTED, "n_isotopes * n_gridpoints >= 2^31");
-    if ((double)p->n_isotopes * (double)(p->n_isotopes * p->n_gridpoints + 63) >= 4294967296.0)
+    if (p->grid_type == GF_GRID_UNIONIZED &&
+        (double)p->n_isotopes * (double)(p->n_isotopes * p->n_gridpoints + 63) >= 4294967296.0)
       return fail(GF_E_UNSUPPORTED, "index grid larger than 2^32 entries");
   } else {
     if (p->numL != 4) return fail(GF_E_INVAL, "numL must be 4 (got %d)", p->numL);
@@ -160,9 +164,10 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     } else {
       L.scratch_bytes = 256;
     }
+    if (p->n_gridpoints > kMaxSortGp) L.scratch_bytes = std::max(L.scratch_bytes, al(npts * 24));  // big_* sort
     if (p->grid_type == GF_GRID_HASH) {
       L.hg_pitch = (p->hash_bins + 63) & ~63;
-      L.HG = take((size_t)p->n_isotopes * (size_t)L.hg_pitch * 2);
+      L.HG = take((size_t)p->n_isotopes * (size_t)L.hg_pitch * (p->n_gridpoints > kMaxGp16 ? 4 : 2));
     }
   } else {
     const size_t n = (size_t)p->n_isotopes;
@@ -322,6 +327,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       X.n_union = (long long)X.n_iso * X.n_gp;
       X.ig_pitch = L.ig_pitch;
       X.hg_pitch = L.hg_pitch;
+      X.hg32 = X.n_gp > kMaxGp16 ? 1 : 0;
       X.total = total;
       double *G = reinterpret_cast<double *>(base + L.G);
       double *Ed = reinterpret_cast<double *>(base + L.Ed);
@@ -339,7 +345,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       put(GF_ARR_ENERGY, Ed, npts * 8, X.n_gp);
       if (U) put(GF_ARR_UNIONIZED, U, npts * 8, (int64_t)npts);
       if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 2, X.ig_pitch);
-      if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * 2, X.hg_pitch);
+      if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * (X.hg32 ? 4 : 2), X.hg_pitch);
       if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
       put(GF_ARR_RECIP_WIDTH, Rd, npts * 8, X.n_gp);
       if (XR) put(GF_ARR_INTERVALS, XR, npts * 128, X.n_gp);

@@ -118,6 +118,122 @@ __global__ void __launch_bounds__(1024) xs_sort_fill(double *__restrict__ G, dou
   }
 }
 
+// ------------------------------------------------------------------------------------------ K0a/b, large n_gp
+// NEXT-2 (XL / XXL point counts): a nuclide's points do not fit one CTA's SMEM
+// sort above kMaxSortGp.  Same result (per-nuclide sort by (E, generation index)) in global passes:
+// keys -> SMEM bitonic sort of kMaxSortGp-point chunks -> stable pairwise merges of runs inside each
+// nuclide's segment -> records regenerated from the sorted generation indices.
+__global__ void __launch_bounds__(256) big_keys(unsigned long long *__restrict__ K, uint32_t *__restrict__ Gn,
+                                                long long npts, int n_gp, uint64_t seed) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= npts) return;
+  uint64_t s = lcg_skip(seed, 6ull * (uint64_t)g);  // point k of nuclide i is draw block i n_gp + k
+  K[g] = (unsigned long long)__double_as_longlong(lcg_draw(s));  // E in [0, 1]: bit order == value order
+  Gn[g] = (uint32_t)(g % n_gp);
+}
+
+// One CTA per (chunk, nuclide): bitonic sort of up to kMaxSortGp (key, gen) pairs in SMEM.
+__global__ void __launch_bounds__(1024) big_chunk_sort(unsigned long long *__restrict__ K, uint32_t *__restrict__ Gn,
+                                                       int n_gp) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(smem);
+  uint32_t *gen = reinterpret_cast<uint32_t *>(key + kMaxSortGp);
+  const int nuc = blockIdx.y;
+  const int c0 = blockIdx.x * kMaxSortGp, len = min(kMaxSortGp, n_gp - c0);
+  const size_t base = (size_t)nuc * n_gp + c0;
+  for (int k = threadIdx.x; k < kMaxSortGp; k += blockDim.x) {
+    key[k] = k < len ? K[base + k] : ~0ull;
+    gen[k] = k < len ? Gn[base + k] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= kMaxSortGp; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (kMaxSortGp >> 1); t += blockDim.x) {
+        const int lo = 2 * stride * (t / stride) + (t % stride), hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const unsigned long long ka = key[lo], kb = key[hi];
+        const uint32_t ga = gen[lo], gb = gen[hi];
+        if (((ka > kb) || (ka == kb && ga > gb)) == asc) {
+          key[lo] = kb;
+          key[hi] = ka;
+          gen[lo] = gb;
+          gen[hi] = ga;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    K[base + k] = key[k];
+    Gn[base + k] = gen[k];
+  }
+}
+
+// Merge sorted runs of length L pairwise inside each nuclide's segment.  Generation indices of a
+// left run all precede the right run's, so "left before equal right" (lower bound for left
+// elements, upper bound for right ones) keeps the (E, gen) order.
+__global__ void __launch_bounds__(256) big_merge_round(const unsigned long long *__restrict__ Ki,
+                                                       const uint32_t *__restrict__ Gi,
+                                                       unsigned long long *__restrict__ Ko, uint32_t *__restrict__ Go,
+                                                       long long npts, int n_gp, int L) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= npts) return;
+  const long long seg = (g / n_gp) * (long long)n_gp;
+  const int loc = (int)(g - seg), run = loc / L, start = run * L;
+  const int pstart = (run ^ 1) * L;
+  const unsigned long long v = Ki[g];
+  int rank = 0, base = start;
+  if (pstart < n_gp) {
+    const int plen = min(L, n_gp - pstart);
+    const unsigned long long *P = Ki + seg + pstart;
+    int lo = 0, hi = plen;
+    if (run & 1) {  // right run: #{left <= v}
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (P[mid] <= v) lo = mid + 1; else hi = mid;
+      }
+    } else {  // left run: #{right < v}
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (P[mid] < v) lo = mid + 1; else hi = mid;
+      }
+    }
+    rank = lo;
+    base = min(start, pstart);
+  }
+  const long long o = seg + base + (loc - start) + rank;
+  Ko[o] = v;
+  Go[o] = Gi[g];
+}
+
+// Records in sorted order, regenerated from the generation index; Ed, Rd and the zero-width flag.
+__global__ void __launch_bounds__(256) big_write(const unsigned long long *__restrict__ K,
+                                                 const uint32_t *__restrict__ Gn, double *__restrict__ Gr,
+                                                 double *__restrict__ Ed, double *__restrict__ Rd,
+                                                 int *__restrict__ zero_width, long long npts, int n_gp,
+                                                 uint64_t seed) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= npts) return;
+  const long long seg = (g / n_gp) * (long long)n_gp;
+  const int k = (int)(g - seg);
+  uint64_t s = lcg_skip(seed, 6ull * (uint64_t)(seg + Gn[g]));
+  double v[6];
+#pragma unroll
+  for (int f = 0; f < 6; f++) v[f] = lcg_draw(s);
+  double2 *rec = reinterpret_cast<double2 *>(Gr + g * 6);
+  rec[0] = make_double2(v[0], v[1]);
+  rec[1] = make_double2(v[2], v[3]);
+  rec[2] = make_double2(v[4], v[5]);
+  Ed[g] = v[0];
+  double r = 0.0;
+  if (k + 1 < n_gp) {
+    const double w = __dsub_rn(__longlong_as_double((long long)K[g + 1]), v[0]);
+    if (!(w >= 0x1p-960)) atomicOr(zero_width, 1);
+    r = __drcp_rn(w);
+  }
+  Rd[g] = r;
+}
+
 // ------------------------------------------------------------------------------------------ K0b'
 // Interval records for the sorted lookup kernel, one 128-B line per interval k < n_gp - 1 of each
 // nuclide (layout in gf_internal.cuh XsDev::XR).  Every stored difference / reciprocal is the RN
@@ -227,8 +343,8 @@ __global__ void ubin_build(const double *__restrict__ U, uint32_t *__restrict__ 
 }
 
 // ------------------------------------------------------------------------------------------ K0e
-__global__ void hg_build(const double *__restrict__ Ed, uint16_t *__restrict__ HG, int n_iso, int n_gp, int bins,
-                         int pitch) {
+__global__ void hg_build(const double *__restrict__ Ed, uint16_t *__restrict__ HG, uint32_t *__restrict__ HG32,
+                         int n_iso, int n_gp, int bins, int pitch) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)n_iso * pitch) return;
   int nuc = (int)(t / pitch), b = (int)(t % pitch);
@@ -238,7 +354,10 @@ __global__ void hg_build(const double *__restrict__ Ed, uint16_t *__restrict__ H
     double energy = __dmul_rn((double)b, du);
     v = bisect<int>(Ed + (size_t)nuc * n_gp, energy, 0, n_gp - 1);
   }
-  HG[(size_t)nuc * pitch + b] = (uint16_t)v;
+  if (HG32)
+    HG32[(size_t)nuc * pitch + b] = (uint32_t)v;  // n_gp > 65536 (XL / XXL)
+  else
+    HG[(size_t)nuc * pitch + b] = (uint16_t)v;
 }
 
 // ------------------------------------------------------------------------------------------ K0f
@@ -256,15 +375,37 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, do
                            double *scratch, cudaStream_t st) {
   cudaError_t e;
   const long long npts = (long long)X.n_iso * X.n_gp;
-  int npow = 2;
-  while (npow < X.n_gp) npow <<= 1;
-  size_t smem = (size_t)npow * (sizeof(unsigned long long) + sizeof(uint32_t));
-  if ((e = cudaFuncSetAttribute(xs_sort_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-    return e;
-  int threads = npow >= 1024 ? 1024 : (npow < 64 ? 64 : npow);
   if ((e = cudaMemsetAsync(zero_width, 0, sizeof(int), st)) != cudaSuccess) return e;
-  xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, Rd, zero_width, X.n_gp, npow, seed);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (X.n_gp <= kMaxSortGp) {
+    int npow = 2;
+    while (npow < X.n_gp) npow <<= 1;
+    size_t smem = (size_t)npow * (sizeof(unsigned long long) + sizeof(uint32_t));
+    if ((e = cudaFuncSetAttribute(xs_sort_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return e;
+    int threads = npow >= 1024 ? 1024 : (npow < 64 ? 64 : npow);
+    xs_sort_fill<<<X.n_iso, threads, smem, st>>>(G, Ed, Rd, zero_width, X.n_gp, npow, seed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else {  // NEXT-2 point counts: chunked sort + segment merges in the init scratch (24 B per point)
+    unsigned long long *K0 = reinterpret_cast<unsigned long long *>(scratch);
+    unsigned long long *K1 = K0 + npts;
+    uint32_t *G0 = reinterpret_cast<uint32_t *>(K1 + npts), *G1 = G0 + npts;
+    big_keys<<<nblk(npts, 256), 256, 0, st>>>(K0, G0, npts, X.n_gp, seed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const size_t smem = (size_t)kMaxSortGp * (sizeof(unsigned long long) + sizeof(uint32_t));
+    if ((e = cudaFuncSetAttribute(big_chunk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    big_chunk_sort<<<dim3((X.n_gp + kMaxSortGp - 1) / kMaxSortGp, X.n_iso), 1024, smem, st>>>(K0, G0, X.n_gp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    for (int L = kMaxSortGp; L < X.n_gp; L <<= 1) {
+      big_merge_round<<<nblk(npts, 256), 256, 0, st>>>(K0, G0, K1, G1, npts, X.n_gp, L);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      unsigned long long *kt = K0; K0 = K1; K1 = kt;
+      uint32_t *gt = G0; G0 = G1; G1 = gt;
+    }
+    big_write<<<nblk(npts, 256), 256, 0, st>>>(K0, G0, G, Ed, Rd, zero_width, npts, X.n_gp, seed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   if (XR) {
     xr_build<<<nblk(npts, 256), 256, 0, st>>>(G, Rd, XR, npts, X.n_gp);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -295,7 +436,9 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, do
     ubin_build<<<nblk(kUBins + 1, 256), 256, 0, st>>>(U, ubin, X.n_union);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   } else if (X.grid_type == GF_GRID_HASH) {
-    hg_build<<<nblk((long long)X.n_iso * X.hg_pitch, 256), 256, 0, st>>>(Ed, HG, X.n_iso, X.n_gp, X.bins, X.hg_pitch);
+    hg_build<<<nblk((long long)X.n_iso * X.hg_pitch, 256), 256, 0, st>>>(
+        Ed, X.hg32 ? nullptr : HG, X.hg32 ? reinterpret_cast<uint32_t *>(HG) : nullptr, X.n_iso, X.n_gp, X.bins,
+        X.hg_pitch);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;

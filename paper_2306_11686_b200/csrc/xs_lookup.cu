@@ -123,9 +123,16 @@ __device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, 
     k = __ldg(X.IG + e.y + (uint32_t)idx);
   } else {
     const double *Ed = X.Ed + e.x;
-    const uint16_t *hg = X.HG + e.y + (uint32_t)idx;
-    const int lo_ = __ldg(hg);
-    const int hi_ = (idx == X.bins - 1) ? n_gp - 1 : (int)__ldg(hg + 1) + 1;
+    int lo_, hi_;
+    if (X.hg32) {  // XL / XXL point counts (NEXT-2): u32 entries
+      const uint32_t *hg = reinterpret_cast<const uint32_t *>(X.HG) + e.y + (uint32_t)idx;
+      lo_ = (int)__ldg(hg);
+      hi_ = (idx == X.bins - 1) ? n_gp - 1 : (int)__ldg(hg + 1) + 1;
+    } else {
+      const uint16_t *hg = X.HG + e.y + (uint32_t)idx;
+      lo_ = __ldg(hg);
+      hi_ = (idx == X.bins - 1) ? n_gp - 1 : (int)__ldg(hg + 1) + 1;
+    }
     if (E <= __ldg(Ed + lo_))
       k = 0;
     else if (E >= __ldg(Ed + hi_))

@@ -169,7 +169,7 @@ __device__ __forceinline__ void load_k(const XsDev &X, uint2 e, const double (&E
 template <int GT>
 __device__ __forceinline__ const void *grid_line(const XsDev &X, uint2 e, uint32_t ix) {
   if (GT == GF_GRID_UNIONIZED) return X.IG + e.y + ix;
-  return X.HG + e.y + ix;
+  return X.hg32 ? (const void *)(reinterpret_cast<const uint32_t *>(X.HG) + e.y + ix) : (const void *)(X.HG + e.y + ix);
 }
 
 #ifndef GF_LOCAL_SORT

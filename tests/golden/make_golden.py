@@ -25,6 +25,35 @@ def chunked(o, n, chunk):
     return raw
 
 
+def extra():
+    """Later configs (merged into the existing file): C6 XL hash grid (NEXT-2), C5D0 RS 0 K (NEXT-3),
+    H2 / H3 / H5 history mode (NEXT-1) at full size."""
+    res = json.load(open(OUT))
+    t = time.time()
+    o = O.XSOracle(355, 238847, O.HASH, bins=10000)
+    raw = chunked(o, 17_000_000, 5_000_000)
+    res["C6"] = {"n_iso": 355, "n_gp": 238847, "grid": O.HASH, "n": 17_000_000, "raw": raw, "hash": raw % O.HASH_MOD}
+    print("C6", res["C6"], f"{time.time() - t:.1f}s", flush=True)
+    del o
+    rs0 = O.RSOracle(355, 1000, 100, 4, doppler=0)
+    raw = chunked(rs0, 10_200_000, 1_000_000)
+    res["C5D0"] = {"n_iso": 355, "doppler": 0, "n": 10_200_000, "raw": raw, "hash": raw % O.HASH_MOD}
+    print("C5D0", res["C5D0"], f"{time.time() - t:.1f}s", flush=True)
+    del rs0
+    for name, n_iso in (("H2", 68), ("H3", 355)):
+        o = O.XSOracle(n_iso, 11303, O.UNIONIZED)
+        raw = o.history_batch(0, 500_000, 34)
+        res[name] = {"n_iso": n_iso, "grid": O.UNIONIZED, "particles": 500_000, "L": 34, "raw": raw,
+                     "hash": raw % O.HASH_MOD}
+        print(name, res[name], f"{time.time() - t:.1f}s", flush=True)
+        del o
+    rs = O.RSOracle(355, 1000, 100, 4)
+    raw = rs.history_batch(0, 300_000, 34)
+    res["H5"] = {"n_iso": 355, "particles": 300_000, "L": 34, "raw": raw, "hash": raw % O.HASH_MOD}
+    print("H5", res["H5"], f"{time.time() - t:.1f}s", flush=True)
+    json.dump(res, open(OUT, "w"), indent=1)
+
+
 def main():
     res = {"_source": "oracle/ (plain C, -O2 -ffp-contract=off) via tests/golden/make_golden.py; no CUDA code involved",
            "threads": O.max_threads()}
@@ -53,4 +82,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    extra() if "--extra" in sys.argv else main()

@@ -108,7 +108,7 @@ def test_grid_bytes_closed_form():
 
 
 @pytest.mark.parametrize("field,value,status", [
-    ("abi_version", 2, 1), ("n_isotopes", 0, 1), ("n_gridpoints", 1, 1), ("n_gridpoints", 20000, 4),
+    ("abi_version", 2, 1), ("n_isotopes", 0, 1), ("n_gridpoints", 1, 1), ("n_gridpoints", 70000, 4), ("n_gridpoints", 2 ** 20 + 1, 4),
     ("grid_type", 3, 1), ("n_isotopes", 70, 1)])
 def test_invalid_params(field, value, status):
     p = gf.Params.xsbench()
@@ -176,3 +176,16 @@ def test_history_argument_checks():
     assert L.gf_xs_history_batch(None, 0, 10, 34, 1070, 0, None, None, None, 0, None) == 1
     b = C.c_size_t()
     assert L.gf_xs_history_bytes(None, 10, 0, C.byref(b)) == 1
+
+
+def test_large_gridpoint_counts_accepted():
+    """NEXT-2: XL point counts (238,847 per nuclide) are accepted for the hash and nuclide grids, with
+    u32 hash-grid entries; the unionized grid stays limited to 65,536 (u16 index grid)."""
+    for gt in (gf.NUCLIDE, gf.HASH):
+        st, gb, sb = _bytes(gf.Params.xsbench(355, 238847, gt))
+        assert st == 0
+        assert sb >= 355 * 238847 * 24  # chunked grid sort scratch
+    st, gb, _ = _bytes(gf.Params.xsbench(355, 238847, gf.HASH))
+    npts = 355 * 238847
+    assert gb > npts * (48 + 8 + 8 + 128) + 355 * 10048 * 4
+    assert _bytes(gf.Params.xsbench(68, 65536, gf.UNIONIZED))[0] == 0

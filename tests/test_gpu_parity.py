@@ -532,3 +532,29 @@ def test_integer_material_thresholds(gf, torch):
     for m in range(1, 12):
         s = int(S[m])
         assert float(s) * 2.0 ** -63 >= T[m] and float(s - 1) * 2.0 ** -63 < T[m], m
+
+
+@pytest.mark.parametrize("grid_type,n_iso,n_gp", [(0, 5, 40000), (1, 4, 40000), (2, 5, 40000), (2, 3, 70000),
+                                                   (0, 3, 70000)])
+def test_large_gridpoint_grids(gf, torch, grid_type, n_iso, n_gp):
+    """NEXT-2 point counts: grids above the one-CTA SMEM sort (chunked sort + segment merges) and, above
+    65,536 points, u32 hash-grid entries.  Arrays and lookups bit-identical to the oracle."""
+    o, g = make_pair(gf, n_iso, n_gp, grid_type, bins=997, custom=True)
+    check_arrays(o, g)
+    for sort in (True, False):
+        check_lookups(o, g, 0, 30_001, sort=sort)
+
+
+@pytest.mark.parametrize("grid_type", [0, 2])
+def test_xl_gridpoints(gf, torch, grid_type):
+    """XSBench XL point count (238,847 per nuclide) with the 68-nuclide
+    tables: energy column and hash grid identical to the oracle's, 200 k lookups bit-exact."""
+    o, g = make_pair(gf, 68, 238847, grid_type)
+    Ed = g.array("energy")[0].cpu().numpy().reshape(68, 238847)
+    assert np.array_equal(Ed, o.nuclide_grid()[:, :, 0])
+    if grid_type == O.HASH:
+        HG, pitch = g.array("hash_grid")
+        HG = HG.cpu().numpy().reshape(68, pitch)[:, :10000]
+        assert np.array_equal(HG.T, o.hash_grid())
+    raw = check_lookups(o, g, 5_000_000, 200_000)
+    assert check_lookups(o, g, 5_000_000, 200_000, sort=False) == raw

@@ -62,7 +62,8 @@ typedef struct {
     uint32_t abi_version;   /* must equal GF_XS_ABI_VERSION */
     int32_t bench;          /* gf_bench */
     int32_t n_isotopes;     /* 68 = small, 355 = large (built-in tables); any >= 1 with custom tables */
-    int64_t n_gridpoints;   /* XS: gridpoints per nuclide, 11303 in both sizes; 2 <= n <= 16384 */
+    int64_t n_gridpoints;   /* XS: gridpoints per nuclide, 11303 in both sizes (XL 238,847); 2 <= n <= 2^20;
+                               the unionized grid needs <= 65,536 points per nuclide per band */
     int32_t grid_type;      /* XS: gf_grid_type */
     int32_t hash_bins;      /* XS hash grid: bins (10000); >= 1 */
     int32_t avg_n_poles;    /* RS: average poles per nuclide (1000); >= 1 */
@@ -75,6 +76,14 @@ typedef struct {
     const int32_t *num_nucs;/* NULL = built-in Hoogenboom-Martin tables; else HOST int32[12] ...   */
     const int32_t *mats;    /* ... and HOST int32[12 * max_num_nucs] row-major nuclide ids        */
     int32_t max_num_nucs;   /* row length of `mats` when custom tables are given                  */
+    int32_t n_bands;        /* NEXT-2 energy-band sharding of the UNIONIZED grid: 1 = whole grid     */
+    int32_t band;           /* (default).  With W = n_bands > 1 this grid replica holds the unionized */
+                            /* energies and index grid of band r = `band` only: E in [r/W, (r+1)/W),   */
+                            /* band 0 open below, band W-1 open above; the nuclide grid stays whole.   */
+                            /* Its lookup calls process only the lookups whose E falls in the band, so */
+                            /* W replicas (one per GPU) sum to the whole batch.  Needed when the whole */
+                            /* index grid does not fit (XL: 355 x 84.8 M entries).  Sorted event       */
+                            /* lookups only (GF_SORT_LOCALITY); other calls GF_E_UNSUPPORTED.          */
 } gf_xs_params;
 
 /* Fills *p with the defaults of BASELINE.json configs[2] (XSBench large, unionized) for

@@ -44,14 +44,16 @@ class Params(C.Structure):
                 ("n_gridpoints", C.c_int64), ("grid_type", C.c_int32), ("hash_bins", C.c_int32),
                 ("avg_n_poles", C.c_int32), ("avg_n_windows", C.c_int32), ("numL", C.c_int32),
                 ("doppler", C.c_int32), ("init_seed", C.c_uint64), ("num_nucs", C.c_void_p),
-                ("mats", C.c_void_p), ("max_num_nucs", C.c_int32)]
+                ("mats", C.c_void_p), ("max_num_nucs", C.c_int32), ("n_bands", C.c_int32), ("band", C.c_int32)]
 
     @classmethod
-    def xsbench(cls, n_isotopes=355, n_gridpoints=11303, grid_type=UNIONIZED, hash_bins=10000, seed=42):
+    def xsbench(cls, n_isotopes=355, n_gridpoints=11303, grid_type=UNIONIZED, hash_bins=10000, seed=42,
+                n_bands=1, band=0):
         p = cls()
         _check(lib().gf_xs_default_params(XSBENCH, C.byref(p)))
         p.n_isotopes, p.n_gridpoints, p.grid_type, p.hash_bins, p.init_seed = (
             n_isotopes, n_gridpoints, grid_type, hash_bins, seed)
+        p.n_bands, p.band = n_bands, band
         return p
 
     @classmethod

@@ -4,6 +4,8 @@
 // carving the caller's buffers into arrays, uploading the built-in / custom
 // material tables, and enqueueing the kernels of xs_grid.cu / xs_lookup.cu / rs.cu.  No arithmetic
 // of the method runs here.
+#include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -101,6 +103,8 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   // XS
   size_t G, Ed, Rd, XR, flags, U, IG, HG, ubin;
+  size_t k0, binfo;  // NEXT-2 band grid: k0 / cnt / first [3][n_iso] u32, band info 16 B
+  int band_cap;      // in-band points per nuclide the layout holds
   long long ig_pitch;
   int hg_pitch;
   // RS
@@ -109,6 +113,15 @@ struct Layout {
   size_t thr, moff, mnuc, mconc;
   size_t total_bytes, scratch_bytes;
 };
+
+// In-band points per nuclide the layout provisions: LCG gridpoint energies are iid U[0, 1), so the
+// count is Binomial(n_gp, 1/W); mean + 12 sd + 64 (checked at init, GF_E_UNSUPPORTED if exceeded).
+static int band_capacity(const gf_xs_params *p) {
+  if (p->n_bands <= 1) return (int)p->n_gridpoints;
+  const double n = (double)p->n_gridpoints, w = 1.0 / p->n_bands;
+  const double c = n * w + 12.0 * sqrt(n * w * (1.0 - w)) + 64.0;
+  return (int)std::min(n, std::ceil(c));
+}
 
 static gf_status validate(const gf_xs_params *p) {
   if (!p) return fail(GF_E_INVAL, "params is NULL");
@@ -120,16 +133,20 @@ static gf_status validate(const gf_xs_params *p) {
     if (p->n_gridpoints < 2) return fail(GF_E_INVAL, "n_gridpoints %lld < 2", (long long)p->n_gridpoints);
     if (p->n_gridpoints > kMaxGp)
       return fail(GF_E_UNSUPPORTED, "n_gridpoints %lld > %d", (long long)p->n_gridpoints, kMaxGp);
-    if (p->grid_type == GF_GRID_UNIONIZED && p->n_gridpoints > kMaxGp16)
-      return fail(GF_E_UNSUPPORTED, "unionized grid with n_gridpoints %lld > %d (u16 index grid; its %lld-entry "
-                  "index grid would not fit anyway): use the hash or nuclide grid", (long long)p->n_gridpoints,
-                  kMaxGp16, (long long)p->n_isotopes * p->n_isotopes * p->n_gridpoints);
+    if (p->n_bands < 1 || p->band < 0 || p->band >= p->n_bands)
+      return fail(GF_E_INVAL, "band %d of n_bands %d", p->band, p->n_bands);
+    if (p->n_bands > 1 && p->grid_type != GF_GRID_UNIONIZED)
+      return fail(GF_E_INVAL, "energy bands shard the unionized grid only (grid_type %d)", p->grid_type);
+    if (p->grid_type == GF_GRID_UNIONIZED && (p->n_bands > 1 ? band_capacity(p) + 2 > 65535
+                                                              : p->n_gridpoints > kMaxGp16))
+      return fail(GF_E_UNSUPPORTED, "unionized grid with %d points per nuclide per band (u16 index grid): "
+                  "use more energy bands (n_bands), or the hash or nuclide grid", band_capacity(p));
     if (p->grid_type < 0 || p->grid_type > 2) return fail(GF_E_INVAL, "grid_type %d", p->grid_type);
     if (p->grid_type == GF_GRID_HASH && p->hash_bins < 1) return fail(GF_E_INVAL, "hash_bins %d < 1", p->hash_bins);
     if ((long long)p->n_isotopes * p->n_gridpoints >= (1ll << 31))
       return fail(GF_E_UNSUPPORTED, "n_isotopes * n_gridpoints >= 2^31");
     if (p->grid_type == GF_GRID_UNIONIZED &&
-        (double)p->n_isotopes * (double)(p->n_isotopes * p->n_gridpoints + 63) >= 4294967296.0)
+        (double)p->n_isotopes * (double)(p->n_isotopes * (double)band_capacity(p) + 66) >= 4294967296.0)
       return fail(GF_E_UNSUPPORTED, "index grid larger than 2^32 entries");
   } else {
     if (p->numL != 4) return fail(GF_E_INVAL, "numL must be 4 (got %d)", p->numL);
@@ -156,11 +173,19 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.flags = take(16);
     if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128);
     if (p->grid_type == GF_GRID_UNIONIZED) {
-      L.ig_pitch = (long long)((npts + 63) & ~size_t(63));
-      L.U = take(npts * 8);
+      // whole grid: all n_iso n_gp energies; band: <= band_cap per nuclide plus the two sentinels
+      L.band_cap = band_capacity(p);
+      const size_t nu = p->n_bands > 1 ? (size_t)p->n_isotopes * L.band_cap + 2 : npts;
+      L.ig_pitch = (long long)((nu + 63) & ~size_t(63));
+      L.U = take(nu * 8);
       L.IG = take((size_t)p->n_isotopes * (size_t)L.ig_pitch * 2);
       L.ubin = take((size_t)(kUBins + 1) * 4);
       L.scratch_bytes = al(npts * 8);
+      if (p->n_bands > 1) {
+        L.k0 = take((size_t)p->n_isotopes * 12);
+        L.binfo = take(16);
+        L.scratch_bytes = std::max(L.scratch_bytes, al((size_t)p->n_isotopes * L.band_cap * 16));
+      }
     } else {
       L.scratch_bytes = 256;
     }
@@ -239,6 +264,8 @@ gf_status gf_xs_default_params(int32_t bench, gf_xs_params *p) {
   p->avg_n_windows = 100;
   p->numL = 4;
   p->doppler = 1;
+  p->n_bands = 1;
+  p->band = 0;
   p->init_seed = 42;
   if (bench != GF_XSBENCH && bench != GF_RSBENCH) return fail(GF_E_INVAL, "bench %d", bench);
   return GF_OK;
@@ -340,10 +367,14 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
       X.G = G; X.Ed = Ed; X.Rd = Rd; X.XR = XR; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
-      const size_t npts = (size_t)X.n_union;
+      const bool banded = X.grid_type == GF_GRID_UNIONIZED && p->n_bands > 1;
+      X.k0 = banded ? reinterpret_cast<uint32_t *>(base + L.k0) : nullptr;
+      const double inf = 1.0 / 0.0;
+      X.band_lo = (banded && p->band > 0) ? (double)p->band / (double)p->n_bands : -inf;
+      X.band_hi = (banded && p->band < p->n_bands - 1) ? (double)(p->band + 1) / (double)p->n_bands : inf;
+      const size_t npts = (size_t)X.n_iso * X.n_gp;
       put(GF_ARR_NUCLIDE_GRID, G, npts * 48, X.n_gp);
       put(GF_ARR_ENERGY, Ed, npts * 8, X.n_gp);
-      if (U) put(GF_ARR_UNIONIZED, U, npts * 8, (int64_t)npts);
       if (IG) put(GF_ARR_INDEX_GRID, IG, (size_t)X.n_iso * X.ig_pitch * 2, X.ig_pitch);
       if (HG) put(GF_ARR_HASH_GRID, HG, (size_t)X.n_iso * X.hg_pitch * (X.hg32 ? 4 : 2), X.hg_pitch);
       if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
@@ -351,6 +382,22 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       if (XR) put(GF_ARR_INTERVALS, XR, npts * 128, X.n_gp);
       ce = launch_xs_grid(X, G, Ed, Rd, XR, zero_width, U, IG, HG, ubin, mconc, p->init_seed,
                           static_cast<double *>(scratch), st);
+      if (ce == cudaSuccess && banded) {  // NEXT-2: the band's U (sync: its length sizes the index grid)
+        uint32_t *binfo = reinterpret_cast<uint32_t *>(base + L.binfo);
+        uint32_t *kk = const_cast<uint32_t *>(X.k0);
+        ce = launch_band_union(X, L.band_cap, kk, kk + X.n_iso, U, binfo, static_cast<double *>(scratch), st);
+        uint32_t info[4] = {0, 0, 0, 0};
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(info, binfo, 16, cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (ce == cudaSuccess && info[1]) {
+          delete g;
+          return fail(GF_E_UNSUPPORTED, "a nuclide has more than %d points in band %d of %d (layout bound)",
+                      L.band_cap, p->band, p->n_bands);
+        }
+        X.n_union = (long long)info[0] + 2;
+        if (ce == cudaSuccess) ce = launch_band_index(X, U, IG, ubin, st);
+      }
+      if (U) put(GF_ARR_UNIONIZED, U, (size_t)X.n_union * 8, (int64_t)X.n_union);
       // the exact reciprocal division is used only if no interval has zero (or underflowing) width
       int zw = 1;
       if (ce == cudaSuccess) ce = cudaMemcpyAsync(&zw, zero_width, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -556,6 +603,8 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
   if (n >= (1ull << 32)) return fail(GF_E_INVAL, "n = %llu >= 2^32: split the job into batches", (unsigned long long)n);
   const bool energies = E != nullptr;
   if (energies && !mat) return fail(GF_E_INVAL, "mat is NULL");
+  if (g->p.bench == GF_XSBENCH && g->p.n_bands > 1 && (energies || !(flags & GF_SORT_LOCALITY) || (flags & GF_HOST_IO)))
+    return fail(GF_E_UNSUPPORTED, "energy-band grids serve sorted, device-resident event lookups only");
   const bool host_io = (flags & GF_HOST_IO) != 0;
   BatchLayout B;
   plan_batch(g, n, flags, macro_out != nullptr, energies, B);
@@ -662,6 +711,8 @@ gf_status gf_xs_history_batch(const gf_xs_grid *g, uint64_t first_particle, uint
     if (!g) return fail(GF_E_INVAL, "grid is NULL");
     if (!d_vsum) return fail(GF_E_INVAL, "vsum is NULL");
     if (flags & ~(uint32_t)(GF_SORT_LOCALITY | GF_HIST_WAVES)) return fail(GF_E_INVAL, "unknown flags 0x%x", flags);
+    if (g->p.bench == GF_XSBENCH && g->p.n_bands > 1)
+      return fail(GF_E_UNSUPPORTED, "history mode on an energy-band grid (a particle's lookups cross bands)");
     const int L = lookups_per_particle;
     if (L < 1 || L > (1 << 20)) return fail(GF_E_INVAL, "lookups_per_particle = %d outside [1, 2^20]", L);
     if (n_particles >= (1ull << 32)) return fail(GF_E_INVAL, "n_particles >= 2^32: split the job");

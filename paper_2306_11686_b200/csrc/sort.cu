@@ -7,7 +7,8 @@
 // sort_scatter (sample again, atomic cursor, store E and the lookup position).  Sampling is
 // index-addressed (lookup i draws from fast_forward(seed, 2i)): a thread skips once and steps
 // through kRun consecutive lookups; the material roll is decided on the integer LCG state
-// (pick_material_state, exact).  Measured alternative: a two-level sort (coarse
+// (pick_material_state, exact).  A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi
+// (the defaults keep all).  Measured alternative: a two-level sort (coarse
 // buckets per CTA run, then a per-bucket fine sort) moved fewer DRAM bytes but was not faster.
 #include "gf_internal.cuh"
 
@@ -16,11 +17,19 @@ namespace gf {
 #ifndef GF_DIAG_SCATTER
 #define GF_DIAG_SCATTER 0
 #endif
-constexpr int kRun = 16;  // consecutive lookups per thread in the sampling kernels
+constexpr int kRun = 16;
+
+// Band filter of a NEXT-2 band grid: [lo, hi).  The defaults (-inf, +inf) mean "no band" and keep
+// every lookup, +-inf and NaN energies included.
+__device__ __forceinline__ bool in_band(double E, double lo, double hi) {
+  const bool whole = lo == -__longlong_as_double(0x7ff0000000000000ll) && hi == __longlong_as_double(0x7ff0000000000000ll);
+  return whole || (E >= lo && E < hi);
+}  // consecutive lookups per thread in the sampling kernels
 __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
-                                                  const double *__restrict__ thr, uint32_t *__restrict__ counts) {
+                                                  const double *__restrict__ thr, uint32_t *__restrict__ counts,
+                                                  double band_lo, double band_hi) {
   __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
   if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   __syncthreads();
@@ -42,7 +51,7 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
       s = lcg_next(s);
       mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
     }
-    atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
+    if (in_band(E, band_lo, band_hi)) atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
   }
 }
 
@@ -103,7 +112,8 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
                                                     const double *__restrict__ src_E,
                                                     const uint8_t *__restrict__ src_mat,
                                                     const double *__restrict__ thr, uint32_t *__restrict__ cursor,
-                                                    double *__restrict__ Es, uint32_t *__restrict__ idx) {
+                                                    double *__restrict__ Es, uint32_t *__restrict__ idx,
+                                                    double band_lo, double band_hi) {
   __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
   if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   __syncthreads();
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
         s = lcg_next(s);
         mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
       }
-      pos[r] = (uint32_t)(mat * kNB + sort_bin(E[r]));
+      pos[r] = in_band(E[r], band_lo, band_hi) ? (uint32_t)(mat * kNB + sort_bin(E[r])) : 0xFFFFFFFFu;
     }
   }
 #if GF_DIAG_SCATTER == 1  // diagnostic (wrong results): stores at a hash position, no atomics
@@ -139,11 +149,11 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
 #else
 #pragma unroll
   for (int r = 0; r < kRun; r++)
-    if (r < cnt) pos[r] = atomicAdd(cursor + pos[r], 1u);
+    if (r < cnt && pos[r] != 0xFFFFFFFFu) pos[r] = atomicAdd(cursor + pos[r], 1u);
 #endif
 #pragma unroll
   for (int r = 0; r < kRun; r++) {
-    if (r < cnt) {
+    if (r < cnt && pos[r] != 0xFFFFFFFFu) {  // (outside the band: dropped)
 #if GF_DIAG_SCATTER == 2  // diagnostic (wrong results): atomics only, no stores
       if (E[r] < -1.0)
 #endif
@@ -157,17 +167,18 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 
 cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, double band_lo, double band_hi) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * kBins, st)) != cudaSuccess) return e;
   unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
-  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts);
+  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   scan_local<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   scan_add<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr);
+  sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr,
+                                band_lo, band_hi);
   return cudaGetLastError();
 }
 

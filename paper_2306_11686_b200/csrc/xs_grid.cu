@@ -294,7 +294,7 @@ __global__ void merge_round(const double *__restrict__ in, double *__restrict__ 
 // (pitch % 64 == 0): 4 x 16-B stores per thread.
 __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, const double *__restrict__ U,
                                                 uint16_t *__restrict__ IG, int n_gp, long long n_union,
-                                                long long pitch) {
+                                                long long pitch, const uint32_t *__restrict__ k0) {
   const int nuc = blockIdx.y;
   long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 32;
   if (e0 >= pitch) return;
@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, c
     int v = c - 1;
     v = v < 0 ? 0 : v;
     v = v > n_gp - 2 ? n_gp - 2 : v;
+    if (k0) v -= (int)k0[nuc];  // band grid: relative to the nuclide's interval at the band's low edge
     if (k & 1) w[k >> 1] |= (uint32_t)v << 16; else w[k >> 1] = (uint32_t)v;
   }
   uint4 *dst = reinterpret_cast<uint4 *>(IG + (size_t)nuc * pitch + e0);
@@ -414,7 +415,7 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, do
   concs_fill<<<nblk(X.total, 256), 256, 0, st>>>(mconc, X.total, seed, 6ull * (uint64_t)npts);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-  if (X.grid_type == GF_GRID_UNIONIZED) {
+  if (X.grid_type == GF_GRID_UNIONIZED && !X.k0) {  // (band grids: launch_band_union / _index)
     int rounds = 0;
     for (long long L = X.n_gp; L < npts; L <<= 1) rounds++;
     if (rounds == 0) {
@@ -431,7 +432,7 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, do
       }
     }
     dim3 grid(nblk(X.ig_pitch, 256 * 32), X.n_iso);
-    ig_build<<<grid, 256, 0, st>>>(Ed, U, IG, X.n_gp, X.n_union, X.ig_pitch);
+    ig_build<<<grid, 256, 0, st>>>(Ed, U, IG, X.n_gp, X.n_union, X.ig_pitch, nullptr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ubin_build<<<nblk(kUBins + 1, 256), 256, 0, st>>>(U, ubin, X.n_union);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -442,6 +443,92 @@ cudaError_t launch_xs_grid(const XsDev &X, double *G, double *Ed, double *Rd, do
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ------------------------------------------------------------------------------------------ NEXT-2 bands
+// Energy-band sharding of the unionized grid (SURVEY.md Sec. 8(e) alternative, 8(f) NEXT-2): the band
+// [lo, hi) keeps U_band = {lo} + sorted {A : lo <= A < hi} + {hi} and the index grid over it.  For a
+// lookup E in the band, #{U_band <= E} - 1 indexes the last U_band entry <= E, and every grid point
+// <= E is either < lo or in U_band, so IG_band[u] = clamp(#{A <= E} - 1, 0, n_gp - 2) - k0 with k0 the
+// interval at lo (the sentinels keep u inside [0, n_band - 2] for every E in the band).  The record
+// base of each table entry adds k0, so the lookup kernels are unchanged; results are identical.
+__global__ void band_counts(const double *__restrict__ Ed, int n_iso, int n_gp, double lo, double hi, int cap,
+                            uint32_t *__restrict__ k0, uint32_t *__restrict__ first, uint32_t *__restrict__ cnt,
+                            uint32_t *__restrict__ info) {
+  const int nuc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (nuc >= n_iso) return;
+  const double *A = Ed + (size_t)nuc * n_gp;
+  auto count_lt = [&](double q) {  // #{A < q}
+    int l = 0, h = n_gp;
+    while (l < h) {
+      const int m = (l + h) >> 1;
+      if (A[m] < q) l = m + 1; else h = m;
+    }
+    return l;
+  };
+  int l = 0, h = n_gp;  // #{A <= lo}
+  while (l < h) {
+    const int m = (l + h) >> 1;
+    if (A[m] <= lo) l = m + 1; else h = m;
+  }
+  int k = l - 1;
+  k = k < 0 ? 0 : (k > n_gp - 2 ? n_gp - 2 : k);
+  k0[nuc] = (uint32_t)k;
+  const int a = count_lt(lo), b = count_lt(hi);
+  first[nuc] = (uint32_t)a;
+  cnt[nuc] = (uint32_t)(b - a);
+  atomicAdd(info, (uint32_t)(b - a));
+  if (b - a > cap) atomicOr(info + 1, 1u);  // more points than the layout bound
+}
+
+// Padded runs: run[nuc][j] = A[first + j] for j < cnt, +inf after (sorts last).
+__global__ void band_runs(const double *__restrict__ Ed, int n_iso, int n_gp, int cap,
+                          const uint32_t *__restrict__ first, const uint32_t *__restrict__ cnt,
+                          double *__restrict__ run) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n_iso * cap) return;
+  const int nuc = (int)(t / cap), j = (int)(t % cap);
+  const uint32_t c = min(cnt[nuc], (uint32_t)cap);
+  run[t] = (uint32_t)j < c ? Ed[(size_t)nuc * n_gp + first[nuc] + j] : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+__global__ void band_finish(const double *__restrict__ S, double *__restrict__ U, const uint32_t *__restrict__ info,
+                            double lo, double hi) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long tot = info[0];
+  if (t == 0) U[0] = lo;
+  if (t < tot) U[t + 1] = S[t];
+  if (t == tot) U[tot + 1] = hi;
+}
+
+cudaError_t launch_band_union(const XsDev &X, int cap, uint32_t *k0, uint32_t *cnt, double *U, uint32_t *info,
+                              double *scratch, cudaStream_t st) {
+  cudaError_t e;
+  const long long N = (long long)X.n_iso * cap;
+  uint32_t *first = cnt + X.n_iso;
+  if ((e = cudaMemsetAsync(info, 0, 16, st)) != cudaSuccess) return e;
+  band_counts<<<nblk(X.n_iso, 128), 128, 0, st>>>(X.Ed, X.n_iso, X.n_gp, X.band_lo, X.band_hi, cap, k0, first, cnt,
+                                                  info);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  double *a = scratch, *b = scratch + N;
+  band_runs<<<nblk(N, 256), 256, 0, st>>>(X.Ed, X.n_iso, X.n_gp, cap, first, cnt, a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  for (long long L = cap; L < N; L <<= 1) {
+    merge_round<<<nblk(N, 256), 256, 0, st>>>(a, b, N, L);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    double *t = a; a = b; b = t;
+  }
+  band_finish<<<nblk(N + 2, 256), 256, 0, st>>>(a, U, info, X.band_lo, X.band_hi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_index(const XsDev &X, const double *U, uint16_t *IG, uint32_t *ubin, cudaStream_t st) {
+  cudaError_t e;
+  dim3 grid(nblk(X.ig_pitch, 256 * 32), X.n_iso);
+  ig_build<<<grid, 256, 0, st>>>(X.Ed, U, IG, X.n_gp, X.n_union, X.ig_pitch, X.k0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ubin_build<<<nblk(kUBins + 1, 256), 256, 0, st>>>(U, ubin, X.n_union);
+  return cudaGetLastError();
 }
 
 }  // namespace gf

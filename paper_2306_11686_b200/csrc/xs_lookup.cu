@@ -80,12 +80,14 @@ __device__ __forceinline__ XsTables stage_xs_tables(const XsDev &X, unsigned cha
   for (int t = threadIdx.x; t < X.total; t += blockDim.x) {
     const uint32_t nuc = (uint32_t)X.mnuc[t];
     const double c = X.mconc[t];
+    // record base of the nuclide; a band grid's index grid holds intervals relative to k0[nuc]
+    const uint32_t rb = nuc * (uint32_t)X.n_gp + (X.k0 ? X.k0[nuc] : 0u);
     if (PK) {
       const unsigned long long cb = (unsigned long long)__double_as_longlong(c);
-      s_pk[t] = make_uint4(nuc * (uint32_t)X.n_gp, nuc * pitch, (uint32_t)cb, (uint32_t)(cb >> 32));
+      s_pk[t] = make_uint4(rb, nuc * pitch, (uint32_t)cb, (uint32_t)(cb >> 32));
     } else {
       s_conc[t] = c;
-      s_ent[t] = make_uint2(nuc * (uint32_t)X.n_gp, nuc * pitch);
+      s_ent[t] = make_uint2(rb, nuc * pitch);
     }
   }
   if (threadIdx.x < kMats + 1) s_off[threadIdx.x] = X.moff[threadIdx.x];
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  n = min(n, __ldg(mstart + kMats));  // lookups kept by the sort (band grids keep their band's)
   uint32_t v = 0;
   if (p < n) {
     int mat = 0;
@@ -318,7 +321,8 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
   const size_t smem = xs_table_smem(X.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), st)) != cudaSuccess)
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), st, X.band_lo, X.band_hi)) !=
+        cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
     const int kern = sorted_kernel(n);

@@ -33,9 +33,9 @@ constexpr int kIgPf = 10;  // index-/hash-grid L2 prefetch distance (nuclides)
 // (hash) of lookup p.
 template <int GT>
 __global__ void __launch_bounds__(256) idx_prep(XsDev X, uint32_t n, const double *__restrict__ Es,
-                                                uint32_t *__restrict__ ix) {
+                                                const uint32_t *__restrict__ mstart, uint32_t *__restrict__ ix) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) ix[p] = (uint32_t)energy_index<GT>(X, Es[p]);
+  if (p < min(n, __ldg(mstart + kMats))) ix[p] = (uint32_t)energy_index<GT>(X, Es[p]);
 }
 
 // One interval record of XsDev::XR: v0 = (E[k+1], E[k+1] - E[k]), v(1+c) = (xs_c[k+1],
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
   __shared__ uint32_t ms[kMats + 1];  // material segment starts (SMEM: registers go to the loop)
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
   const XsTables T = stage_xs_tables<GF_PACKTAB>(X, smem);  // (its __syncthreads also publishes ms)
+  n = min(n, ms[kMats]);  // lookups kept by the sort (band grids keep their band's)
   uint32_t vacc = 0;
   const uint32_t ngroups = (n + kL - 1) / kL;
   for (uint32_t g = blockIdx.x * kTpbL + threadIdx.x; g < ngroups; g += gridDim.x * kTpbL) {
@@ -347,7 +348,7 @@ static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t ngroups = (n + kL - 1) / kL;
   const uint32_t grid = min((ngroups + kTpbL - 1) / kTpbL, (uint32_t)(sms * max(blocks_per_sm, 1)));
-  idx_prep<GT><<<nblk(n, 256), 256, 0, st>>>(X, n, S.Es, S.us);
+  idx_prep<GT><<<nblk(n, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum);
   return cudaGetLastError();

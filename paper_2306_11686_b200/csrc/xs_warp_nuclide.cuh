@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_warp_nuclide(XsDev X, ui
   extern __shared__ __align__(128) unsigned char smem[];
   const XsTables T = stage_xs_tables(X, smem);
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  n = min(n, __ldg(mstart + kMats));  // lookups kept by the sort
   const bool act = p < n;
   uint32_t v = 0;
   if (__any_sync(kFull, act)) {  // warp-uniform: every lane of a live warp takes part

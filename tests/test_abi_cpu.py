@@ -189,3 +189,17 @@ def test_large_gridpoint_counts_accepted():
     npts = 355 * 238847
     assert gb > npts * (48 + 8 + 8 + 128) + 355 * 10048 * 4
     assert _bytes(gf.Params.xsbench(68, 65536, gf.UNIONIZED))[0] == 0
+
+
+def test_energy_band_params():
+    """NEXT-2: unionized grids shard by energy band; the XL unionized grid needs >= 4 bands (u16 index
+    grid per band) and its band layout is ~1/W of the whole index grid."""
+    assert _bytes(gf.Params.xsbench(355, 238847, gf.UNIONIZED))[0] == 4
+    assert _bytes(gf.Params.xsbench(355, 238847, gf.UNIONIZED, n_bands=2, band=0))[0] == 4
+    st, gb8, _ = _bytes(gf.Params.xsbench(355, 238847, gf.UNIONIZED, n_bands=8, band=3))
+    assert st == 0
+    ig8 = 355 * (355 * 238847 / 8) * 2
+    assert ig8 < gb8 < ig8 * 1.1 + 355 * 238847 * (48 + 8 + 8 + 128) + 64e6
+    assert _bytes(gf.Params.xsbench(68, 11303, gf.HASH, n_bands=2, band=0))[0] == 1
+    assert _bytes(gf.Params.xsbench(68, 11303, gf.UNIONIZED, n_bands=2, band=2))[0] == 1
+    assert _bytes(gf.Params.xsbench(68, 11303, gf.UNIONIZED, n_bands=4, band=1))[0] == 0

@@ -558,3 +558,52 @@ def test_xl_gridpoints(gf, torch, grid_type):
         assert np.array_equal(HG.T, o.hash_grid())
     raw = check_lookups(o, g, 5_000_000, 200_000)
     assert check_lookups(o, g, 5_000_000, 200_000, sort=False) == raw
+
+
+def band_of(E, W):
+    r = np.floor(np.asarray(E) * W).astype(np.int64)
+    return np.clip(r, 0, W - 1)
+
+
+def check_bands(gf, torch, o, mk_grid, W, first, n):
+    """Run every band replica over the same lookups: each keeps the lookups of its band (rows of the
+    others stay NaN), the raw sums add up to the oracle's, every row equals the oracle's bitwise."""
+    raw_o, m_o = o.lookup_batch(first, n, want_macro=True)
+    E = np.array([O.sample(first + i)[0] for i in range(n)])
+    bands = band_of(E, W)
+    raw_sum = 0
+    for r in range(W):
+        g = mk_grid(r)
+        vs = torch.zeros(1, dtype=torch.int64, device="cuda")
+        m = torch.full((n, 5), float("nan"), dtype=torch.float64, device="cuda")
+        g.lookup_batch_async(first, n, vs, macro_out=m)
+        raw_sum += int(vs.item())
+        m = m.cpu().numpy()
+        mine = bands == r
+        assert np.array_equal(m[mine], m_o[mine]), r
+        assert np.isnan(m[~mine]).all(), r
+        with pytest.raises(gf.GFError):  # unsorted / energies / history calls are refused on band grids
+            g.lookup_batch(0, 10, sort=False)
+        del g
+        torch.cuda.empty_cache()
+    assert raw_sum == raw_o
+
+
+@pytest.mark.parametrize("W", [2, 3, 5])
+def test_energy_bands_small(gf, torch, W):
+    """NEXT-2 energy-band sharding of the unionized grid (tiny custom grid, several bands)."""
+    nn, mats = tiny_tables(5)
+    o = O.XSOracle(5, 4000, O.UNIONIZED, num_nucs=nn, mats=mats)
+    check_bands(gf, torch, o, lambda r: gf.Grid(gf.Params.xsbench(5, 4000, gf.UNIONIZED, n_bands=W, band=r),
+                                                 num_nucs=nn, mats=mats), W, 777, 30_001)
+
+
+def test_energy_bands_unionized_beyond_u16(gf, torch):
+    """100,000 points per nuclide: the whole unionized index grid would need u32 intervals; four bands
+    of ~25 k points each keep u16 and reproduce the oracle (its nuclide grid: identical results)."""
+    o = O.XSOracle(68, 100_000, O.NUCLIDE)
+    assert gf.lib  # the whole-grid unionized request is refused:
+    with pytest.raises(gf.GFError):
+        gf.Grid(gf.Params.xsbench(68, 100_000, gf.UNIONIZED))
+    check_bands(gf, torch, o, lambda r: gf.Grid(gf.Params.xsbench(68, 100_000, gf.UNIONIZED, n_bands=4, band=r)),
+                4, 1_000_000, 100_000)

@@ -41,6 +41,9 @@ CONFIGS = {
     # NEXT-2 point counts: XSBench XL, 238,847 gridpoints per nuclide (the hash grid: the unionized
     # grid's index grid would be 355 x 84.8 M entries)
     "C6": ("xs", 355, 2, 17_000_000, "XSBench XL 355x238847, hash grid 10000 bins, 17M event lookups (NEXT-2)"),
+    # NEXT-2 energy-band sharding: XSBench XL on the unionized grid, whose index grid (355 x 84.8 M
+    # entries) fits no GPU whole; 8 energy bands, rank r of N serves bands r, r + N, ...
+    "C7": ("xs", 355, 1, 17_000_000, "XSBench XL 355x238847, unionized grid in 8 energy bands, 17M event lookups (NEXT-2)"),
     # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
     "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
     "H3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
@@ -53,7 +56,7 @@ HIST_L = {"H2": 34, "H3": 34, "H5": 34}  # lookups per particle (history configs
 #   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop);
 #   C5D0 (0 K): 55.4 x (51 + 9.09 x 43 per pole: sqrt, two textbook complex divisions, 3 products) ~ 24,500.
 ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
-       "C3N": (0, 1551), "C5D0": (0, 24500), "C6": (6203, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
+       "C3N": (0, 1551), "C5D0": (0, 24500), "C6": (6203, 1551), "C7": (6517, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
 
 
 def oracle_run(o, cfg, first, n, threads):
@@ -167,7 +170,8 @@ def cpu_baseline(cfg_name, seconds=12.0):
     bench, n_iso, gt, n, _ = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
     if bench == "xs":
-        o = O.XSOracle(n_iso, 238847 if cfg_name == "C6" else 11303, gt, bins=10000)
+        o = O.XSOracle(n_iso, 238847 if cfg_name in ("C6", "C7") else 11303, O.NUCLIDE if cfg_name == "C7" else gt,
+                       bins=10000)  # (C7: the nuclide grid gives the unionized grid's results; its IG is 120 GB)
     else:
         o = O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1)
     k = 20_000
@@ -191,7 +195,8 @@ def run_reference(args, rank, world):
     cfg_name = args.config
     bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
-    o = (O.XSOracle(n_iso, 238847 if cfg_name == "C6" else 11303, gt, bins=10000) if bench == "xs"
+    o = (O.XSOracle(n_iso, 238847 if cfg_name in ("C6", "C7") else 11303, O.NUCLIDE if cfg_name == "C7" else gt,
+                    bins=10000) if bench == "xs"
          else O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1))
     t = time.perf_counter()
     _, k0 = oracle_run(o, cfg_name, 0, 20_000, threads)
@@ -220,6 +225,65 @@ def run_reference(args, rank, world):
                              "sample": f"{step_n} consecutive lookups per step out of {n}"},
             "e2e": {"value": v, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_bands(args, rank, world, dev, gf, torch, dist, C):
+    """C7: every rank builds, in turn, the band replicas of its bands (r, r + N, ... of W = 8; grid build
+    untimed), and runs the full event batch through each -- the sort keeps the band's lookups.  A step
+    is one batch through all of the rank's bands; value = 17 M / max-over-ranks step time."""
+    W, n = 8, CONFIGS["C7"][3]
+    mine = list(range(rank, W, world))
+    st = torch.cuda.current_stream()
+    vsum = torch.zeros(1, dtype=torch.int64, device=dev)
+    per_band, raws, builds = [], 0, 0.0
+    for b in mine:
+        t0 = time.perf_counter()
+        grid = gf.Grid(gf.Params.xsbench(355, 238847, gf.UNIONIZED, n_bands=W, band=b), device=dev)
+        builds += time.perf_counter() - t0
+        sc = torch.empty(grid.scratch_bytes(n, gf.SORT_LOCALITY), dtype=torch.uint8, device=dev)
+        ts = []
+        for k in range(args.warmup + args.steps):
+            vsum.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gf._check(gf.lib().gf_xs_lookup_batch(grid.h, 0, n, gf.STARTING_SEED, gf.SORT_LOCALITY, None,
+                                                  C.c_void_p(vsum.data_ptr()), C.c_void_p(sc.data_ptr()),
+                                                  sc.numel(), C.c_void_p(st.cuda_stream)))
+            e1.record()
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                ts.append(e0.elapsed_time(e1))
+        raws += int(vsum.item())
+        per_band.append(statistics.median(ts))
+        del grid, sc
+        torch.cuda.empty_cache()
+    step_ms = sum(per_band)
+    rv = torch.tensor([raws], dtype=torch.int64, device=dev)
+    if dist is not None:
+        dist.all_reduce(rv)
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t.item()
+    if rank == 0:
+        peaks = load_peaks()
+        look_s = step_ms * 1e-3
+        roof = {"bound": "alu", "kernel": "sort + idx_prep + xs_lookup_group<unionized> per band",
+                "achieved": 1551 * n / look_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
+                "unit": "TFLOP/s", "traffic": None,
+                "note": "1551 fp64 flops/lookup x 17 M lookups / summed band step time (each band re-samples and "
+                        "sorts all 17 M lookups, keeping its own)"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        line = {"metric": "lookups/sec", "value": n / look_s, "unit": "lookups/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
+                "config": {"workload": f"C7: {CONFIGS['C7'][4]}", "n_lookups": n, "bands": W,
+                           "bands_per_rank": len(mine), "band_ms": per_band,
+                           "parallelism": f"energy bands over {world} rank(s), 1 int64 all-reduce"},
+                "roofline": roof, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": args.steps * len(mine) * 6, "hash": gf.verify(int(rv.item())),
+                "raw": int(rv.item()), "grid_build_s": builds}
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -264,6 +328,12 @@ def main():
             dist.init_process_group(backend)
         dist.barrier()
     dev = torch.device("cuda", local)
+    if args.config == "C7":
+        bench_bands(args, rank, world, dev, gf, torch, dist, C)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     bench, n_iso, gt, n_total, desc = CONFIGS[args.config]
     if args.scaling == "weak":
         first, n = gf.weak_range(n_total, rank)

@@ -89,3 +89,15 @@ def test_rs_history_all_modes(gf, n_iso, n_p):
         assert raw_g == raw_o, mode
         err = np.abs(m_g.cpu().numpy() - m_o) / S[..., None]
         assert err.max() <= 1e-10, (mode, err.max())
+
+
+def test_history_full_size_goldens(gf):
+    """H2 / H3 (XSBench small / large, 500 k particles x 34) and H5 (RSBench large, 300 k x 34): whole-run
+    raw sums against the oracle's (tests/golden/make_golden.py --extra)."""
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_hashes.json")))
+    for name, n_iso in (("H2", 68), ("H3", 355)):
+        g = gf.Grid(gf.Params.xsbench(n_iso, 11303, gf.UNIONIZED))
+        assert g.history_batch(0, 500_000, 34) == gold[name]["raw"], name
+        del g
+    r = gf.Grid(gf.Params.rsbench(355))
+    assert r.history_batch(0, 300_000, 34) == gold["H5"]["raw"]

@@ -607,3 +607,44 @@ def test_energy_bands_unionized_beyond_u16(gf, torch):
         gf.Grid(gf.Params.xsbench(68, 100_000, gf.UNIONIZED))
     check_bands(gf, torch, o, lambda r: gf.Grid(gf.Params.xsbench(68, 100_000, gf.UNIONIZED, n_bands=4, band=r)),
                 4, 1_000_000, 100_000)
+
+
+def test_full_size_golden_C6_C5D0(gf, torch):
+    """Whole-batch raw sums against the oracle's full-size values (tests/golden/make_golden.py --extra):
+    C6 XSBench XL hash grid, 17 M lookups (NEXT-2); C5D0 RSBench 0 K, 10.2 M lookups (NEXT-3)."""
+    gold = golden()
+    g = gf.Grid(gf.Params.xsbench(355, 238847, gf.HASH))
+    assert g.lookup_batch(0, 17_000_000) == gold["C6"]["raw"]
+    del g
+    torch.cuda.empty_cache()
+    r = gf.Grid(gf.Params.rsbench(355, doppler=0))
+    assert r.lookup_batch(0, 10_200_000) == gold["C5D0"]["raw"]
+
+
+def test_C7_bands_sum_to_xl(gf, torch):
+    """C7: the eight energy-band replicas of the XL unionized grid together reproduce the XL batch's raw
+    sum (the oracle's C6 value: the hash and unionized grids give identical intervals), and one band's
+    per-lookup outputs equal the oracle's nuclide-grid results bitwise."""
+    gold = golden()
+    n, W, raw = 17_000_000, 8, 0
+    for b in range(W):
+        g = gf.Grid(gf.Params.xsbench(355, 238847, gf.UNIONIZED, n_bands=W, band=b))
+        raw += g.lookup_batch(0, n)
+        if b == 3:
+            o = O.XSOracle(355, 238847, O.NUCLIDE)
+            check_bands_one(gf, torch, o, g, W, b, 2_000_000, 50_000)
+            del o
+        del g
+        torch.cuda.empty_cache()
+    assert raw == gold["C6"]["raw"]
+
+
+def check_bands_one(gf, torch, o, g, W, b, first, n):
+    raw_o, m_o = o.lookup_batch(first, n, want_macro=True)
+    E = np.array([O.sample(first + i)[0] for i in range(n)])
+    mine = band_of(E, W) == b
+    vs = torch.zeros(1, dtype=torch.int64, device="cuda")
+    m = torch.full((n, 5), float("nan"), dtype=torch.float64, device="cuda")
+    g.lookup_batch_async(first, n, vs, macro_out=m)
+    m = m.cpu().numpy()
+    assert mine.sum() > 0 and np.array_equal(m[mine], m_o[mine]) and np.isnan(m[~mine]).all()

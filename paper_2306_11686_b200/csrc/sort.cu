@@ -1,7 +1,7 @@
 // sort.cu -- A1/A2: sampling and the locality sort on sm_100a.
 //
-// Lookups are ordered by the key (material, floor(E 2^17)) -- 12 x 2^17 bins, ~18-36 lookups per
-// bin at 17 M -- so that neighbouring lookups share intervals in the lookup kernels; order inside a
+// Lookups are ordered by the key (material, floor(E 2^b)) -- b = 17 at 17 M: 12 x 2^17 bins, ~18-36
+// lookups per bin (smaller batches: fewer bins, sort_bits) -- so that neighbouring lookups share intervals in the lookup kernels; order inside a
 // bin is arbitrary (results are order-independent: integer hash, outputs scattered back through idx).
 // Counting sort: sort_count (sample, one global atomic per lookup on its bin), a two-kernel scan,
 // sort_scatter (sample again, atomic cursor, store E and the lookup position).  Sampling is
@@ -21,6 +21,13 @@ constexpr int kRun = 16;
 
 // Band filter of a NEXT-2 band grid: [lo, hi).  The defaults (-inf, +inf) mean "no band" and keep
 // every lookup, +-inf and NaN energies included.
+// Sort bin of E within its material with 2^nb_log2 bins: floor(E 2^nb_log2) clamped (exact scaling).
+__device__ __forceinline__ int sort_bin_bits(double E, int nb_log2) {
+  int b = (int)__dmul_rn(E, (double)(1 << nb_log2));
+  b = b < 0 ? 0 : b;
+  return b > (1 << nb_log2) - 1 ? (1 << nb_log2) - 1 : b;
+}
+
 __device__ __forceinline__ bool in_band(double E, double lo, double hi) {
   const bool whole = lo == -__longlong_as_double(0x7ff0000000000000ll) && hi == __longlong_as_double(0x7ff0000000000000ll);
   return whole || (E >= lo && E < hi);
@@ -29,7 +36,7 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
-                                                  double band_lo, double band_hi) {
+                                                  double band_lo, double band_hi, int nb_log2) {
   __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
   if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   __syncthreads();
@@ -51,7 +58,7 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
       s = lcg_next(s);
       mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
     }
-    if (in_band(E, band_lo, band_hi)) atomicAdd(counts + mat * kNB + sort_bin(E), 1u);
+    if (in_band(E, band_lo, band_hi)) atomicAdd(counts + (mat << nb_log2) + sort_bin_bits(E, nb_log2), 1u);
   }
 }
 
@@ -86,9 +93,9 @@ __global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restric
 
 // Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n).
 __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ cursor, const uint32_t *__restrict__ btot,
-                                                     uint32_t *__restrict__ mstart) {
+                                                     uint32_t *__restrict__ mstart, int nb_log2) {
   __shared__ uint32_t s_off;
-  constexpr int nblocks = kBins / kScanBlk;
+  const int nblocks = (kMats << nb_log2) / kScanBlk;
   if (threadIdx.x < 32) {
     uint32_t acc = 0;
     for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) acc += btot[i];
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ curs
   const int b = blockIdx.x * kScanBlk + threadIdx.x;
   const uint32_t v = cursor[b] + s_off;
   cursor[b] = v;
-  if (b % kNB == 0) mstart[b / kNB] = v;
+  if ((b & ((1 << nb_log2) - 1)) == 0) mstart[b >> nb_log2] = v;
 }
 
 __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
                                                     const uint8_t *__restrict__ src_mat,
                                                     const double *__restrict__ thr, uint32_t *__restrict__ cursor,
                                                     double *__restrict__ Es, uint32_t *__restrict__ idx,
-                                                    double band_lo, double band_hi) {
+                                                    double band_lo, double band_hi, int nb_log2) {
   __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
   if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   __syncthreads();
@@ -139,7 +146,8 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
         s = lcg_next(s);
         mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
       }
-      pos[r] = in_band(E[r], band_lo, band_hi) ? (uint32_t)(mat * kNB + sort_bin(E[r])) : 0xFFFFFFFFu;
+      pos[r] = in_band(E[r], band_lo, band_hi) ? (uint32_t)((mat << nb_log2) + sort_bin_bits(E[r], nb_log2))
+                                               : 0xFFFFFFFFu;
     }
   }
 #if GF_DIAG_SCATTER == 1  // diagnostic (wrong results): stores at a hash position, no atomics
@@ -165,20 +173,31 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
 
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
+// Bins per material: 2^17 for dense batches (17 M: ~18-36 lookups per fuel / water bin), fewer for
+// small ones so that the zeroing and the two scans over 12 x 2^b counters stay small next to the batch
+// (a 500 k-lookup history wave: 2^14), i.e. ~4 lookups per bin of the average material, b in [10, 17].
+static int sort_bits(uint32_t n) {
+  int b = 10;
+  while (b < 17 && ((uint64_t)kMats << (b + 2)) < n) b++;
+  return b;
+}
+
 cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
                                  cudaStream_t st, double band_lo, double band_hi) {
   cudaError_t e;
-  if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * kBins, st)) != cudaSuccess) return e;
+  const int nbl = sort_bits(n);
+  const int bins = kMats << nbl;  // a multiple of kScanBlk for nbl >= 10
+  if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
   unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
-  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi);
+  sort_count<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_local<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
+  scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_add<<<kBins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart);
+  scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, nbl);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr,
-                                band_lo, band_hi);
+                                band_lo, band_hi, nbl);
   return cudaGetLastError();
 }
 

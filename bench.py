@@ -515,6 +515,16 @@ def main():
                         f"(SURVEY 8(d)); >1 means the sort removed algorithmic bytes ({peaks['src']})"}
             if prof and prof.get("dram_bytes"):
                 roof_hbm["dram_GBps_measured"] = prof["dram_bytes"] / look_avg_s / 1e9
+        roof_gather = None
+        if alg_bytes and peaks.get("gather96_GBps"):
+            # the north_star's "fraction of the HBM random-gather roofline" (SURVEY.md 8(d) R-ROOF rho_thru):
+            # whole-step lookups/s x the random-order sector bytes per lookup / the measured random 96-B
+            # record-pair gather bandwidth (tools/roofline_probe.cu, K6); > 1 because the sort removes the gather
+            gb = value / world * alg_bytes / 1e9
+            roof_gather = {"bound": "gather", "achieved": gb, "peak": peaks["gather96_GBps"], "unit": "GB/s",
+                           "frac": gb / peaks["gather96_GBps"],
+                           "note": f"R-ROOF rho_thru: per-GPU lookups/s x {alg_bytes} B / measured random 96-B "
+                                   f"record-pair gather bandwidth ({peaks['probe_src']})"}
         cb = None
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_baseline(args.config)
@@ -530,7 +540,8 @@ def main():
                        "parallelism": f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, {first + n}) on rank 0), "
                                       f"grid replicated, 1 int64 "
                                       f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
-            "roofline": roof, "roofline_hbm_model": roof_hbm, "cpu_baseline": cb, "e2e": e2e,
+            "roofline": roof, "roofline_hbm_model": roof_hbm, "roofline_gather": roof_gather,
+            "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY) if not HL else
                                  (1 if args.hist_mode == "direct" else
                                   HL * (1 + launches_per_step(bench, gt, flags & gf.SORT_LOCALITY)))),

@@ -7,8 +7,8 @@ S=$O/status.txt; : > $S
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest=$? $(tail -1 $O/pytest_gpu.log)" >> $S
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke=$?" >> $S
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench_default=$?" >> $S
-for c in C1 C2 C4 C5 C5D0 C3N H2 H3 H5; do
-  timeout 600 python bench.py --config $c --steps 5 --no-e2e --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench_$c=$?" >> $S
+for c in C1 C2 C4 C5 C5D0 C3N C6 C7 H2 H3 H5; do
+  timeout 900 python bench.py --config $c --steps 5 --no-e2e --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench_$c=$?" >> $S
 done
 timeout 300 python bench.py --config C3 --steps 3 --no-sort --no-e2e --no-cpu-baseline > $O/bench_C3_nosort.json 2> $O/bench_C3_nosort.err; echo "bench_C3_nosort=$?" >> $S
 timeout 300 python bench.py --impl reference --config C3 --steps 2 --warmup 1 > $O/bench_reference_C3.json 2> $O/bench_reference_C3.err; echo "reference=$?" >> $S

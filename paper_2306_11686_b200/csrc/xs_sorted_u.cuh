@@ -31,11 +31,25 @@ constexpr int kIgPf = 10;  // index-/hash-grid L2 prefetch distance (nuclides)
 
 // A3 for every sorted lookup in a separate, massively parallel pass: ix[p] = u (unionized) or b
 // (hash) of lookup p.
+// Four consecutive sorted lookups per thread: one 32-B energy load, one 16-B index store, and their
+// searches are independent (their probes overlap in flight; neighbours hit the same U lines).
 template <int GT>
 __global__ void __launch_bounds__(256) idx_prep(XsDev X, uint32_t n, const double *__restrict__ Es,
                                                 const uint32_t *__restrict__ mstart, uint32_t *__restrict__ ix) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < min(n, __ldg(mstart + kMats))) ix[p] = (uint32_t)energy_index<GT>(X, Es[p]);
+  n = min(n, __ldg(mstart + kMats));
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (p + 4 <= n) {
+    double e0, e1, e2, e3;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(e0), "=d"(e1), "=d"(e2), "=d"(e3) : "l"(Es + p));
+    uint4 r;
+    r.x = (uint32_t)energy_index<GT>(X, e0);
+    r.y = (uint32_t)energy_index<GT>(X, e1);
+    r.z = (uint32_t)energy_index<GT>(X, e2);
+    r.w = (uint32_t)energy_index<GT>(X, e3);
+    *reinterpret_cast<uint4 *>(ix + p) = r;
+  } else {
+    for (uint32_t q = p; q < n; q++) ix[q] = (uint32_t)energy_index<GT>(X, Es[q]);
+  }
 }
 
 // One interval record of XsDev::XR: v0 = (E[k+1], E[k+1] - E[k]), v(1+c) = (xs_c[k+1],
@@ -348,7 +362,7 @@ static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t ngroups = (n + kL - 1) / kL;
   const uint32_t grid = min((ngroups + kTpbL - 1) / kTpbL, (uint32_t)(sms * max(blocks_per_sm, 1)));
-  idx_prep<GT><<<nblk(n, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
+  idx_prep<GT><<<nblk(((long long)n + 3) / 4, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum);
   return cudaGetLastError();

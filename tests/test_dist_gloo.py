@@ -67,3 +67,43 @@ def test_weak_ranges_tile_the_batch():
     assert [f for f, _ in rs] == [0, n, 2 * n] and all(c == n for _, c in rs)
     o = O.XSOracle(68, 11303, O.NUCLIDE)
     assert sum(o.lookup_batch(f, c, threads=1) for f, c in rs) == o.lookup_batch(0, world * n, threads=1)
+
+
+def _band_worker(rank, world, port, W, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import numpy as np
+    import oracle as O
+    from paper_2306_11686_b200 import dist as gdist
+    o = O.XSOracle(68, 11303, O.NUCLIDE)
+    E = np.array([O.sample(i)[0] for i in range(n)])
+    band = np.clip(np.floor(E * W).astype(np.int64), 0, W - 1)
+    raw = 0
+    for b in range(rank, W, world):  # bench.py C7: rank r serves bands r, r + N, ...
+        idx = np.flatnonzero(band == b).astype(np.uint64)
+        if len(idx):
+            raw += o.lookup_indices(idx)[0]
+    vsum = torch.tensor([raw], dtype=torch.int64)
+    gdist.reduce_raw(vsum)
+    if rank == 0:
+        q.put(int(vsum.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_energy_bands_partition_the_batch():
+    """NEXT-2 band sharding over ranks (bench.py C7): every lookup belongs to exactly one of W energy
+    bands, ranks serve bands r, r + N, ...; the all-reduced raw sum equals the whole batch's."""
+    import oracle as O
+    W, n, world = 8, 20_000, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, W, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    raw = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert raw == O.XSOracle(68, 11303, O.NUCLIDE).lookup_batch(0, n)

@@ -81,6 +81,12 @@ def lib():
         L.rso_lookup_batch.restype = u64; L.rso_lookup_batch.argtypes = [vp, u64, u64, u64, vp, vp, i32]
         L.rso_lookup_indices.restype = u64; L.rso_lookup_indices.argtypes = [vp, vp, u64, u64, vp, vp]
         L.rso_set_doppler.restype = None; L.rso_set_doppler.argtypes = [vp, i32]
+        L.pro_create.restype = vp; L.pro_create.argtypes = [C.c_long, i32, u64]
+        L.pro_free.restype = None; L.pro_free.argtypes = [vp]
+        L.pro_nnz.restype = C.c_long; L.pro_nnz.argtypes = [vp]
+        L.pro_arrays.restype = None; L.pro_arrays.argtypes = [vp, vp, vp, vp]
+        L.pro_propagate_csr.restype = None; L.pro_propagate_csr.argtypes = [C.c_long, vp, vp, vp, vp, vp, i32]
+        L.pro_propagate.restype = None; L.pro_propagate.argtypes = [vp, vp, vp, i32]
         L.xso_history_batch.restype = u64; L.xso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, i32]
         L.rso_history_batch.restype = u64; L.rso_history_batch.argtypes = [vp, u64, u64, i32, u64, vp, vp, i32]
         _lib = L
@@ -313,3 +319,44 @@ class RSOracle:
         sc = np.zeros((n_p, L)) if want_macro else None
         raw = lib().rso_history_batch(self.h, first_p, n_p, L, seed, _ptr(out), _ptr(sc), threads)
         return (raw, out, sc) if want_macro else raw
+
+
+# ------------------------------------------------------------------ page-rank oracle (NEXT-4)
+class PROracle:
+    """In-edge CSR page-rank graph and propagation step (readings R-PR-GRAPH / R-PR-STEP)."""
+
+    def __init__(self, n, D=16, seed=GRID_SEED):
+        h = lib().pro_create(n, D, seed)
+        if not h:
+            raise ValueError("pro_create rejected the parameters")
+        self.h, self.n, self.D = h, n, D
+        self.nnz = lib().pro_nnz(h)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().pro_free(h)
+            self.h = None
+
+    def arrays(self):
+        rowptr = np.zeros(self.n + 1, dtype=np.int64)
+        col = np.zeros(max(self.nnz, 1), dtype=np.int32)
+        outdeg = np.zeros(self.n, dtype=np.int32)
+        lib().pro_arrays(self.h, _ptr(rowptr), _ptr(col), _ptr(outdeg))
+        return rowptr, col[:self.nnz], outdeg
+
+    def propagate(self, r, threads=0):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        out = np.zeros(self.n, dtype=np.float64)
+        lib().pro_propagate(self.h, _ptr(r), _ptr(out), threads)
+        return out
+
+
+def pr_propagate_csr(rowptr, col, outdeg, r, threads=1):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    outdeg = np.ascontiguousarray(outdeg, dtype=np.int32)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    out = np.zeros(len(rowptr) - 1, dtype=np.float64)
+    lib().pro_propagate_csr(len(rowptr) - 1, _ptr(rowptr), _ptr(col), _ptr(outdeg), _ptr(r), _ptr(out), threads)
+    return out

@@ -806,3 +806,96 @@ int o_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ================================================================ NEXT-4: page-rank propagation
+ * HeCBench page-rank, "the propagation step is measured" (Fig. 9c; SURVEY.md
+ * Sec. 8(f) NEXT-4).  The paper gives no generator or formula; readings R-PR-GRAPH / R-PR-STEP
+ * (DESIGN.md Sec. 3):
+ *   graph: N nodes; node u draws from s = fast_forward(seed, 2 D u): out-degree
+ *          d_u = 1 + floor(lcg_double(&s) * (2 D - 1)), then d_u targets v = floor(lcg_double(&s) * N)
+ *          (clamped to N - 1); in-edges of v are ordered by (u, j) -- j the draw order.
+ *   step:  contrib[u] = r[u] / d_u;  r'[v] = (1 - 0.85) / N + 0.85 * (sum over in-edges in order of
+ *          contrib[u]), every operation fp64 round-to-nearest, sums left to right. */
+typedef struct {
+    long n, nnz;
+    int D;
+    long *rowptr;   /* [n + 1] in-edge CSR by destination */
+    int32_t *col;   /* [nnz] source of each in-edge */
+    int32_t *outdeg;/* [n] */
+} pr_oracle;
+
+pr_oracle *pro_create(long n, int D, uint64_t seed) {
+    if (n < 1 || D < 1) return NULL;
+    pr_oracle *o = (pr_oracle *)calloc(1, sizeof(pr_oracle));
+    o->n = n;
+    o->D = D;
+    o->outdeg = (int32_t *)malloc(sizeof(int32_t) * n);
+    o->rowptr = (long *)calloc((size_t)n + 1, sizeof(long));
+    /* pass 1: degrees and in-degree counts */
+    for (long u = 0; u < n; u++) {
+        uint64_t s = o_fast_forward(seed, 2ULL * (uint64_t)D * (uint64_t)u);
+        int d = 1 + (int)(o_lcg_double(&s) * (double)(2 * D - 1));
+        if (d > 2 * D - 1) d = 2 * D - 1;
+        o->outdeg[u] = d;
+        for (int j = 0; j < d; j++) {
+            long v = (long)(o_lcg_double(&s) * (double)n);
+            if (v > n - 1) v = n - 1;
+            o->rowptr[v + 1]++;
+        }
+    }
+    for (long v = 0; v < n; v++) o->rowptr[v + 1] += o->rowptr[v];
+    o->nnz = o->rowptr[n];
+    o->col = (int32_t *)malloc(sizeof(int32_t) * (size_t)(o->nnz > 0 ? o->nnz : 1));
+    long *fill = (long *)malloc(sizeof(long) * n);
+    memcpy(fill, o->rowptr, sizeof(long) * n);
+    /* pass 2: sources in (u, j) order -- appending in generation order keeps rows sorted */
+    for (long u = 0; u < n; u++) {
+        uint64_t s = o_fast_forward(seed, 2ULL * (uint64_t)D * (uint64_t)u);
+        (void)o_lcg_double(&s);
+        for (int j = 0; j < o->outdeg[u]; j++) {
+            long v = (long)(o_lcg_double(&s) * (double)n);
+            if (v > n - 1) v = n - 1;
+            o->col[fill[v]++] = (int32_t)u;
+        }
+    }
+    free(fill);
+    return o;
+}
+
+void pro_free(pr_oracle *o) {
+    if (!o) return;
+    free(o->rowptr);
+    free(o->col);
+    free(o->outdeg);
+    free(o);
+}
+
+long pro_nnz(const pr_oracle *o) { return o->nnz; }
+void pro_arrays(const pr_oracle *o, long *rowptr, int32_t *col, int32_t *outdeg) {
+    memcpy(rowptr, o->rowptr, sizeof(long) * (o->n + 1));
+    memcpy(col, o->col, sizeof(int32_t) * o->nnz);
+    memcpy(outdeg, o->outdeg, sizeof(int32_t) * o->n);
+}
+
+/* R-PR-STEP on any in-edge CSR (also used by the pins with hand-made graphs). */
+void pro_propagate_csr(long n, const long *rowptr, const int32_t *col, const int32_t *outdeg, const double *r,
+                       double *out, int nthreads) {
+    double *contrib = (double *)malloc(sizeof(double) * n);
+    const double base = (1.0 - 0.85) / (double)n;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+    for (long u = 0; u < n; u++) contrib[u] = r[u] / (double)outdeg[u];
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (long v = 0; v < n; v++) {
+        double s = 0.0;
+        for (long e = rowptr[v]; e < rowptr[v + 1]; e++) s = s + contrib[col[e]];
+        out[v] = base + 0.85 * s;
+    }
+    free(contrib);
+}
+
+void pro_propagate(const pr_oracle *o, const double *r, double *out, int nthreads) {
+    pro_propagate_csr(o->n, o->rowptr, o->col, o->outdeg, r, out, nthreads);
+}

@@ -44,6 +44,8 @@ CONFIGS = {
     # NEXT-2 energy-band sharding: XSBench XL on the unionized grid, whose index grid (355 x 84.8 M
     # entries) fits no GPU whole; 8 energy bands, rank r of N serves bands r, r + N, ...
     "C7": ("xs", 355, 1, 17_000_000, "XSBench XL 355x238847, unionized grid in 8 energy bands, 17M event lookups (NEXT-2)"),
+    # NEXT-4: page-rank propagation step (HeCBench page-rank), 2^24 nodes, out-degree 16
+    "P1": ("pr", 1 << 24, 16, 0, "page-rank propagation step, 2^24 nodes, average out-degree 16 (NEXT-4)"),
     # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
     "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
     "H3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
@@ -195,6 +197,28 @@ def run_reference(args, rank, world):
     cfg_name = args.config
     bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
+    if bench == "pr":  # page-rank: whole propagation steps of the same graph
+        import numpy as np
+        o = O.PROracle(n_iso, gt)
+        r = np.full(n_iso, 1.0 / n_iso)
+        for _ in range(args.warmup):
+            r = o.propagate(r, threads=threads)
+        times = []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = o.propagate(r, threads=threads)
+            times.append(time.perf_counter() - t)
+        v = o.nnz * args.steps / sum(times)
+        line = {"impl": "reference", "metric": "edges/sec", "value": v, "unit": "edges/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (LCG-generated graph, seed 42; uniform initial ranks)",
+                "config": {"workload": f"{cfg_name}: {desc}", "nodes": n_iso, "edges": o.nnz},
+                "cpu_baseline": {"value": v, "unit": "edges/s", "cores": threads, "kind": "oracle",
+                                 "sample": "whole propagation steps"},
+                "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     o = (O.XSOracle(n_iso, 238847 if cfg_name in ("C6", "C7") else 11303, O.NUCLIDE if cfg_name == "C7" else gt,
                     bins=10000) if bench == "xs"
          else O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1))
@@ -286,6 +310,87 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
         print(json.dumps(line), flush=True)
 
 
+def bench_pagerank(args, rank, world, dev, gf, torch, dist):
+    """P1 (NEXT-4): one step = contributions + in-edge gather over the whole graph (include/gf_pr.h).
+    Every rank runs its own replica (weak scaling; independent problems, no exchange)."""
+    import numpy as np
+    n, D = CONFIGS["P1"][1], CONFIGS["P1"][2]
+    t0 = time.perf_counter()
+    g = gf.PRGraph(n, D, device=dev.index)
+    build_s = time.perf_counter() - t0
+    nnz = g.n_edges
+    a = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    b = torch.empty_like(a)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.warmup + args.steps)]
+    clocks = ClockSampler(dev.index)
+    ts = []
+    with clocks:
+        if dist is not None:
+            dist.barrier()
+        for k, (e0, e1) in enumerate(evs):
+            flush.fill_(k & 0xFF)
+            e0.record()
+            g.propagate(a, b)
+            e1.record()
+            a, b = b, a
+        torch.cuda.synchronize()
+    ts = [e0.elapsed_time(e1) for e0, e1 in evs[args.warmup:]]
+    step_ms = sum(ts) / len(ts)
+    if dist is not None:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t.item()
+    # end to end through the public API: ranks in from pinned host memory, result back
+    e2e = None
+    if not args.no_e2e:
+        rh = torch.full((n,), 1.0 / n, dtype=torch.float64).pin_memory()
+        oh = torch.empty((n,), dtype=torch.float64).pin_memory()
+        reps = 3
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            a.copy_(rh, non_blocking=True)
+            g.propagate(a, b)
+            oh.copy_(b, non_blocking=True)
+            torch.cuda.synchronize()
+        el = (time.perf_counter() - t0) / reps
+        e2e = {"value": world * nnz / el, "unit": "edges/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "path": "PRGraph.propagate: rank vector H2D, step, result D2H; host-timed"}
+    if rank == 0:
+        peaks = load_peaks()
+        alg = 12 * nnz + 32 * n  # col (4 B) + contribution gather (8 B useful) per edge; 32 B per node
+        gbs = alg / (step_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "pr_contrib + pr_gather", "achieved": gbs, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                "note": f"algorithmic bytes per step = 12 x {nnz} edges + 32 x {n} nodes / mean step time "
+                        f"(CUDA events on the launch stream); peak {peaks['src']}"}
+        cb = None
+        if not args.no_cpu_baseline and world == 1:
+            import oracle as O
+            threads = len(os.sched_getaffinity(0))
+            o = O.PROracle(n, D)
+            r = np.full(n, 1.0 / n)
+            o.propagate(r, threads=threads)
+            t0 = time.perf_counter()
+            o.propagate(r, threads=threads)
+            dt = time.perf_counter() - t0
+            cb = {"value": o.nnz / dt, "unit": "edges/s", "cores": threads, "kind": "oracle",
+                  "sample": f"one full propagation step of the same graph ({o.nnz} edges), plain C oracle, "
+                            f"OpenMP {threads} threads, {dt:.2f} s"}
+        line = {"metric": "edges/sec", "value": world * nnz / (step_ms * 1e-3), "unit": "edges/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (LCG-generated graph, seed 42; uniform initial ranks)",
+                "config": {"workload": f"P1: {CONFIGS['P1'][4]}", "nodes": n, "edges": nnz,
+                           "l2": "flushed between steps by a 256 MiB write (outside events)",
+                           "parallelism": f"independent replicas x{world}"},
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": 2 * args.steps,
+                "clocks": clocks.summary(), "graph_build_s": build_s}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -328,8 +433,11 @@ def main():
             dist.init_process_group(backend)
         dist.barrier()
     dev = torch.device("cuda", local)
-    if args.config == "C7":
-        bench_bands(args, rank, world, dev, gf, torch, dist, C)
+    if args.config in ("C7", "P1"):
+        if args.config == "C7":
+            bench_bands(args, rank, world, dev, gf, torch, dist, C)
+        else:
+            bench_pagerank(args, rank, world, dev, gf, torch, dist)
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()

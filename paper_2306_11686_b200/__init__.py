@@ -16,7 +16,7 @@ import os
 
 from .build import LIB as _LIB_PATH
 
-__all__ = ["Params", "Grid", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
+__all__ = ["Params", "Grid", "PRGraph", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
            "SORT_LOCALITY", "HISTORY", "HOST_IO", "HIST_WAVES", "HASH_MOD", "STARTING_SEED", "shard_range", "weak_range", "GFError"]
 
 XSBENCH, RSBENCH = 0, 1
@@ -94,6 +94,12 @@ def lib():
             "gf_xs_grid_info": (i32, [vp, P(i32)]),
             "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
             "gf_xs_last_error": (C.c_char_p, []),
+            "gf_pr_graph_bytes": (i32, [C.c_int64, i32, P(sz), P(sz)]),
+            "gf_pr_graph_init": (i32, [C.c_int64, i32, u64, C.c_int, vp, sz, vp, sz, vp, P(vp)]),
+            "gf_pr_graph_free": (i32, [vp]),
+            "gf_pr_graph_info": (i32, [vp, P(C.c_int64), P(vp), P(vp), P(vp)]),
+            "gf_pr_propagate": (i32, [vp, vp, vp, vp, vp]),
+            "gf_pr_last_error": (C.c_char_p, []),
             "gf_xs_version": (C.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -302,3 +308,67 @@ class Grid:
         self.history_batch_async(first_p, n_p, vsum, L, seed, mode, macro, stream)
         raw = int(vsum.item())
         return (raw, macro) if want_macro else raw
+
+
+# ------------------------------------------------------------------ page-rank (NEXT-4, include/gf_pr.h)
+def _pr_check(status: int):
+    if status != 0:
+        raise GFError(status, lib().gf_pr_last_error().decode())
+
+
+class PRGraph:
+    """Page-rank graph built on the GPU (readings R-PR-GRAPH / R-PR-STEP); ``propagate`` runs one step."""
+
+    def __init__(self, n_nodes: int, avg_degree: int = 16, seed: int = 42, device=None, stream=None):
+        import torch
+        self.torch = torch
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.device, self.n = dev, n_nodes
+        gb, sb = C.c_size_t(), C.c_size_t()
+        _pr_check(lib().gf_pr_graph_bytes(n_nodes, avg_degree, C.byref(gb), C.byref(sb)))
+        self.buf = torch.empty(gb.value, dtype=torch.uint8, device=dev)
+        scratch = torch.empty(sb.value, dtype=torch.uint8, device=dev)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            _pr_check(lib().gf_pr_graph_init(n_nodes, avg_degree, seed, dev.index, C.c_void_p(self.buf.data_ptr()),
+                                             gb.value, C.c_void_p(scratch.data_ptr()), sb.value,
+                                             _stream_ptr(torch, stream), C.byref(h)))
+        del scratch
+        self.h = h
+        ne = C.c_int64()
+        _pr_check(lib().gf_pr_graph_info(self.h, C.byref(ne), None, None, None))
+        self.n_edges = ne.value
+        self.contrib = torch.empty(n_nodes, dtype=torch.float64, device=dev)
+
+    def arrays(self):
+        """(rowptr u32 [N+1], col u32 [nnz], outdeg i32 [N]) as int64 CPU numpy arrays (tests)."""
+        import numpy as np
+        torch = self.torch
+        rp, cl, od = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _pr_check(lib().gf_pr_graph_info(self.h, None, C.byref(rp), C.byref(cl), C.byref(od)))
+        base = self.buf.data_ptr()
+
+        def view(p, count, dt):
+            off = p.value - base
+            return self.buf[off:off + count * 4].view(dt).cpu().numpy()
+        return (view(rp, self.n + 1, torch.int32).astype(np.int64) & 0xFFFFFFFF,
+                view(cl, self.n_edges, torch.int32).astype(np.int64) & 0xFFFFFFFF, view(od, self.n, torch.int32))
+
+    def propagate(self, r_in, r_out=None, stream=None):
+        torch = self.torch
+        if r_out is None:
+            r_out = torch.empty_like(r_in)
+        _pr_check(lib().gf_pr_propagate(self.h, C.c_void_p(r_in.data_ptr()), C.c_void_p(r_out.data_ptr()),
+                                        C.c_void_p(self.contrib.data_ptr()), _stream_ptr(torch, stream)))
+        return r_out
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().gf_pr_graph_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -203,3 +203,23 @@ def test_energy_band_params():
     assert _bytes(gf.Params.xsbench(68, 11303, gf.HASH, n_bands=2, band=0))[0] == 1
     assert _bytes(gf.Params.xsbench(68, 11303, gf.UNIONIZED, n_bands=2, band=2))[0] == 1
     assert _bytes(gf.Params.xsbench(68, 11303, gf.UNIONIZED, n_bands=4, band=1))[0] == 0
+
+
+def test_pagerank_abi_exports_and_checks():
+    """include/gf_pr.h (NEXT-4): every declared function is exported; argument checks run before any
+    CUDA call."""
+    import os as _os
+    src = open(_os.path.join(_os.path.dirname(HEADER), "gf_pr.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(gf_pr_\w+)\s*\(", src)))
+    assert len(names) == 6
+    out = subprocess.run(["nm", "-D", "--defined-only", gfbuild.LIB], capture_output=True, text=True).stdout
+    assert set(names) <= set(re.findall(r"\bT (gf_pr_\w+)", out))
+    L = gf.lib()
+    gb, sb = C.c_size_t(), C.c_size_t()
+    assert L.gf_pr_graph_bytes(1 << 24, 16, C.byref(gb), C.byref(sb)) == 0
+    assert gb.value >= (1 << 24) * 31 * 4
+    assert L.gf_pr_graph_bytes(0, 16, C.byref(gb), C.byref(sb)) == 1
+    assert L.gf_pr_graph_bytes(100, 33, C.byref(gb), C.byref(sb)) == 1
+    assert L.gf_pr_propagate(None, None, None, None, None) == 1
+    assert L.gf_pr_last_error()

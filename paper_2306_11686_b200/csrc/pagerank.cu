@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kPrTpb) pr_contrib(uint32_t n, const double *_
 
 // kG lanes per row; lane q of the group loads in-edges a + q, a + q + kG, ...; the row's sum is
 // accumulated in row order by walking the group's lanes in turn (one shuffle per edge step).
-constexpr int kG = 4;
+#ifndef GF_PR_G
+#define GF_PR_G 4
+#endif
+constexpr int kG = GF_PR_G;  // lanes per destination row
 
 __global__ void __launch_bounds__(kPrTpb) pr_gather(uint32_t n, const uint32_t *__restrict__ rowptr,
                                                     const uint32_t *__restrict__ col, const double *__restrict__ c,
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kPrTpb) pr_gather(uint32_t n, const uint32_t *
   const int q = (int)(t % kG);
   const bool live = v < n;
   const uint32_t a = live ? __ldg(rowptr + v) : 0u, b = live ? __ldg(rowptr + v + 1) : 0u;
-  const unsigned gmask = 0xFu << ((threadIdx.x & 31) & ~(kG - 1));  // this row's 4 lanes
+  const unsigned gmask = (unsigned)((1ull << kG) - 1) << ((threadIdx.x & 31) & ~(kG - 1));  // this row's lanes
   double s = 0.0;
   // rounds of kG edges: every lane fetches its edge of the round, then the group adds them in order
   for (uint32_t e0 = a; e0 < b; e0 += kG) {

@@ -81,6 +81,9 @@ def lib():
         L.rso_lookup_batch.restype = u64; L.rso_lookup_batch.argtypes = [vp, u64, u64, u64, vp, vp, i32]
         L.rso_lookup_indices.restype = u64; L.rso_lookup_indices.argtypes = [vp, vp, u64, u64, vp, vp]
         L.rso_set_doppler.restype = None; L.rso_set_doppler.argtypes = [vp, i32]
+        L.amo_nnz.restype = C.c_long; L.amo_nnz.argtypes = [i32, i32, i32]
+        L.amo_matrix.restype = None; L.amo_matrix.argtypes = [i32, i32, i32, vp, vp, vp]
+        L.amo_relax.restype = None; L.amo_relax.argtypes = [C.c_long, vp, vp, vp, vp, vp, vp, i32]
         L.pro_create.restype = vp; L.pro_create.argtypes = [C.c_long, i32, u64]
         L.pro_free.restype = None; L.pro_free.argtypes = [vp]
         L.pro_nnz.restype = C.c_long; L.pro_nnz.argtypes = [vp]
@@ -359,4 +362,28 @@ def pr_propagate_csr(rowptr, col, outdeg, r, threads=1):
     r = np.ascontiguousarray(r, dtype=np.float64)
     out = np.zeros(len(rowptr) - 1, dtype=np.float64)
     lib().pro_propagate_csr(len(rowptr) - 1, _ptr(rowptr), _ptr(col), _ptr(outdeg), _ptr(r), _ptr(out), threads)
+    return out
+
+
+# ------------------------------------------------------------------ AMGmk relax oracle (NEXT-4)
+def amg_matrix(nx, ny, nz):
+    """27-point Laplacian CSR (R-AMG-MAT): (rowptr int64, col int32, val float64)."""
+    nnz = lib().amo_nnz(nx, ny, nz)
+    n = nx * ny * nz
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    col = np.zeros(nnz, dtype=np.int32)
+    val = np.zeros(nnz, dtype=np.float64)
+    lib().amo_matrix(nx, ny, nz, _ptr(rowptr), _ptr(col), _ptr(val))
+    return rowptr, col, val
+
+
+def amg_relax(rowptr, col, val, f, u, threads=0):
+    """One Jacobi sweep (R-AMG-RELAX)."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(len(rowptr) - 1)
+    lib().amo_relax(len(rowptr) - 1, _ptr(rowptr), _ptr(col), _ptr(val), _ptr(f), _ptr(u), _ptr(out), threads)
     return out

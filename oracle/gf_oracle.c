@@ -899,3 +899,62 @@ void pro_propagate_csr(long n, const long *rowptr, const int32_t *col, const int
 void pro_propagate(const pr_oracle *o, const double *r, double *out, int nthreads) {
     pro_propagate_csr(o->n, o->rowptr, o->col, o->outdeg, r, out, nthreads);
 }
+
+/* ================================================================ NEXT-4: AMGmk relax
+ * "The first measures only the relax kernel of the original AMGmk proxy application".
+ * Readings R-AMG-MAT / R-AMG-RELAX: the 27-point Laplacian on an nx x ny x nz grid
+ * (row i = x + nx (y + ny z)), CSR with the diagonal (26) first and then the existing neighbours (-1)
+ * in increasing column order; one Jacobi relaxation sweep
+ *     u'[i] = (f[i] - sum_{jj > first} a[jj] u[col[jj]]) / a[first],
+ * fp64 round-to-nearest, the row sum from the right-hand side down, left to right. */
+long amo_nnz(int nx, int ny, int nz) {
+    long c = 0;
+    for (int z = 0; z < nz; z++)
+        for (int y = 0; y < ny; y++)
+            for (int x = 0; x < nx; x++) {
+                int cnt = 0;
+                for (int dz = -1; dz <= 1; dz++)
+                    for (int dy = -1; dy <= 1; dy++)
+                        for (int dx = -1; dx <= 1; dx++) {
+                            int X = x + dx, Y = y + dy, Z = z + dz;
+                            if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) cnt++;
+                        }
+                c += cnt;
+            }
+    return c;
+}
+
+void amo_matrix(int nx, int ny, int nz, long *rowptr, int32_t *col, double *val) {
+    long e = 0, i = 0;
+    rowptr[0] = 0;
+    for (int z = 0; z < nz; z++)
+        for (int y = 0; y < ny; y++)
+            for (int x = 0; x < nx; x++, i++) {
+                col[e] = (int32_t)i;
+                val[e++] = 26.0;
+                for (int dz = -1; dz <= 1; dz++)
+                    for (int dy = -1; dy <= 1; dy++)
+                        for (int dx = -1; dx <= 1; dx++) {
+                            if (!dx && !dy && !dz) continue;
+                            int X = x + dx, Y = y + dy, Z = z + dz;
+                            if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
+                                col[e] = (int32_t)(X + (long)nx * (Y + (long)ny * Z));
+                                val[e++] = -1.0;
+                            }
+                        }
+                rowptr[i + 1] = e;
+            }
+}
+
+void amo_relax(long n, const long *rowptr, const int32_t *col, const double *val, const double *f, const double *u,
+               double *out, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; i++) {
+        double res = f[i];
+        for (long jj = rowptr[i] + 1; jj < rowptr[i + 1]; jj++) res = res - val[jj] * u[col[jj]];
+        out[i] = res / val[rowptr[i]];
+    }
+}

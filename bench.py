@@ -46,6 +46,8 @@ CONFIGS = {
     "C7": ("xs", 355, 1, 17_000_000, "XSBench XL 355x238847, unionized grid in 8 energy bands, 17M event lookups (NEXT-2)"),
     # NEXT-4: page-rank propagation step (HeCBench page-rank), 2^24 nodes, out-degree 16
     "P1": ("pr", 1 << 24, 16, 0, "page-rank propagation step, 2^24 nodes, average out-degree 16 (NEXT-4)"),
+    # NEXT-4: AMGmk relax kernel: one Jacobi sweep, 27-point Laplacian on 256^3
+    "A1": ("amg", 256, 256, 256, "AMGmk relax: Jacobi sweep, 27-point Laplacian on a 256^3 grid (NEXT-4)"),
     # NEXT-1 history-based mode: particles x 34 dependent lookups (gf_xs_history_batch)
     "H2": ("xs", 68, 1, 17_000_000, "XSBench small 68x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
     "H3": ("xs", 355, 1, 17_000_000, "XSBench large 355x11303, unionized, HISTORY mode 500k particles x 34 lookups"),
@@ -197,6 +199,30 @@ def run_reference(args, rank, world):
     cfg_name = args.config
     bench, n_iso, gt, n, desc = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
+    if bench == "amg":  # AMGmk relax: whole sweeps of the same matrix
+        import numpy as np
+        rp, col, val = O.amg_matrix(n_iso, gt, n)
+        rows = len(rp) - 1
+        rng = np.random.default_rng(7)
+        f, u = rng.random(rows), rng.random(rows)
+        for _ in range(args.warmup):
+            u = O.amg_relax(rp, col, val, f, u, threads=threads)
+        times = []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            u = O.amg_relax(rp, col, val, f, u, threads=threads)
+            times.append(time.perf_counter() - t)
+        v = len(col) * args.steps / sum(times)
+        line = {"impl": "reference", "metric": "nonzeros/sec", "value": v, "unit": "nonzeros/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (27-point Laplacian; seeded uniform f and u)",
+                "config": {"workload": f"{cfg_name}: {desc}", "rows": rows, "nonzeros": len(col)},
+                "cpu_baseline": {"value": v, "unit": "nonzeros/s", "cores": threads, "kind": "oracle",
+                                 "sample": "whole relaxation sweeps"},
+                "e2e": {"value": v, "unit": "nonzeros/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     if bench == "pr":  # page-rank: whole propagation steps of the same graph
         import numpy as np
         o = O.PROracle(n_iso, gt)
@@ -391,6 +417,83 @@ def bench_pagerank(args, rank, world, dev, gf, torch, dist):
         print(json.dumps(line), flush=True)
 
 
+def bench_amg(args, rank, world, dev, gf, torch, dist):
+    """A1 (NEXT-4): one relaxation sweep over the whole matrix (include/gf_amg.h); replicas per rank."""
+    import numpy as np
+    nx, ny, nz = CONFIGS["A1"][1:4]
+    A = gf.AMGMatrix(nx, ny, nz, device=dev.index)
+    n, nnz = A.n, A.nnz
+    rng = np.random.default_rng(7)
+    f = torch.from_numpy(rng.random(n)).to(dev)
+    a = torch.from_numpy(rng.random(n)).to(dev)
+    b = torch.empty_like(a)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.warmup + args.steps)]
+    clocks = ClockSampler(dev.index)
+    with clocks:
+        if dist is not None:
+            dist.barrier()
+        for k, (e0, e1) in enumerate(evs):
+            flush.fill_(k & 0xFF)
+            e0.record()
+            A.relax(f, a, b)
+            e1.record()
+            a, b = b, a
+        torch.cuda.synchronize()
+    step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs[args.warmup:]) / args.steps
+    if dist is not None:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t.item()
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.from_numpy(rng.random(n)).pin_memory()
+        oh = torch.empty((n,), dtype=torch.float64).pin_memory()
+        reps = 3
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            a.copy_(uh, non_blocking=True)
+            A.relax(f, a, b)
+            oh.copy_(b, non_blocking=True)
+            torch.cuda.synchronize()
+        el = (time.perf_counter() - t0) / reps
+        e2e = {"value": world * nnz / el, "unit": "nonzeros/s", "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n, "path": "AMGMatrix.relax: iterate H2D, sweep, result D2H; host-timed"}
+    if rank == 0:
+        peaks = load_peaks()
+        alg = 12 * nnz + 28 * n  # col (4 B) + value (8 B) per nonzero; rowptr, f, u (diagonal row) and out per row
+        gbs = alg / (step_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "amg_relax", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                "note": f"algorithmic bytes per sweep = 12 x {nnz} nonzeros + 28 x {n} rows / mean sweep time "
+                        f"(CUDA events); the stencil's u gathers hit in cache; peak {peaks['src']}"}
+        cb = None
+        if not args.no_cpu_baseline and world == 1:
+            import oracle as O
+            threads = len(os.sched_getaffinity(0))
+            rp, col, val = O.amg_matrix(nx, ny, nz)
+            fh, uh2 = f.cpu().numpy(), rng.random(n)
+            O.amg_relax(rp, col, val, fh, uh2, threads=threads)
+            t0 = time.perf_counter()
+            O.amg_relax(rp, col, val, fh, uh2, threads=threads)
+            dt = time.perf_counter() - t0
+            cb = {"value": nnz / dt, "unit": "nonzeros/s", "cores": threads, "kind": "oracle",
+                  "sample": f"one full sweep of the same matrix ({nnz} nonzeros), plain C oracle, OpenMP {threads} "
+                            f"threads, {dt:.2f} s"}
+        line = {"metric": "nonzeros/sec", "value": world * nnz / (step_ms * 1e-3), "unit": "nonzeros/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (27-point Laplacian; seeded uniform f and u)",
+                "config": {"workload": f"A1: {CONFIGS['A1'][4]}", "rows": n, "nonzeros": nnz,
+                           "l2": "flushed between sweeps by a 256 MiB write (outside events)",
+                           "parallelism": f"independent replicas x{world}"},
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,11 +536,13 @@ def main():
             dist.init_process_group(backend)
         dist.barrier()
     dev = torch.device("cuda", local)
-    if args.config in ("C7", "P1"):
+    if args.config in ("C7", "P1", "A1"):
         if args.config == "C7":
             bench_bands(args, rank, world, dev, gf, torch, dist, C)
-        else:
+        elif args.config == "P1":
             bench_pagerank(args, rank, world, dev, gf, torch, dist)
+        else:
+            bench_amg(args, rank, world, dev, gf, torch, dist)
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()

@@ -16,7 +16,7 @@ import os
 
 from .build import LIB as _LIB_PATH
 
-__all__ = ["Params", "Grid", "PRGraph", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
+__all__ = ["Params", "Grid", "PRGraph", "AMGMatrix", "verify", "lib", "XSBENCH", "RSBENCH", "NUCLIDE", "UNIONIZED", "HASH",
            "SORT_LOCALITY", "HISTORY", "HOST_IO", "HIST_WAVES", "HASH_MOD", "STARTING_SEED", "shard_range", "weak_range", "GFError"]
 
 XSBENCH, RSBENCH = 0, 1
@@ -100,6 +100,12 @@ def lib():
             "gf_pr_graph_info": (i32, [vp, P(C.c_int64), P(vp), P(vp), P(vp)]),
             "gf_pr_propagate": (i32, [vp, vp, vp, vp, vp]),
             "gf_pr_last_error": (C.c_char_p, []),
+            "gf_amg_matrix_bytes": (i32, [i32, i32, i32, P(sz), P(C.c_int64)]),
+            "gf_amg_matrix_init": (i32, [i32, i32, i32, C.c_int, vp, sz, vp, P(vp)]),
+            "gf_amg_matrix_free": (i32, [vp]),
+            "gf_amg_matrix_info": (i32, [vp, P(C.c_int64), P(C.c_int64), P(vp), P(vp), P(vp)]),
+            "gf_amg_relax": (i32, [vp, vp, vp, vp, vp]),
+            "gf_amg_last_error": (C.c_char_p, []),
             "gf_xs_version": (C.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -365,6 +371,63 @@ class PRGraph:
     def close(self):
         if getattr(self, "h", None) and self.h.value:
             lib().gf_pr_graph_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ AMGmk relax (NEXT-4, include/gf_amg.h)
+def _amg_check(status: int):
+    if status != 0:
+        raise GFError(status, lib().gf_amg_last_error().decode())
+
+
+class AMGMatrix:
+    """27-point Laplacian built on the GPU (R-AMG-MAT); ``relax`` runs one Jacobi sweep (R-AMG-RELAX)."""
+
+    def __init__(self, nx: int, ny: int, nz: int, device=None, stream=None):
+        import torch
+        self.torch = torch
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.device, self.n = dev, nx * ny * nz
+        b, nnz = C.c_size_t(), C.c_int64()
+        _amg_check(lib().gf_amg_matrix_bytes(nx, ny, nz, C.byref(b), C.byref(nnz)))
+        self.nnz = nnz.value
+        self.buf = torch.empty(b.value, dtype=torch.uint8, device=dev)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            _amg_check(lib().gf_amg_matrix_init(nx, ny, nz, dev.index, C.c_void_p(self.buf.data_ptr()), b.value,
+                                                _stream_ptr(torch, stream), C.byref(h)))
+            (stream or torch.cuda.current_stream()).synchronize()
+        self.h = h
+
+    def arrays(self):
+        import numpy as np
+        torch = self.torch
+        rp, cl, vl = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _amg_check(lib().gf_amg_matrix_info(self.h, None, None, C.byref(rp), C.byref(cl), C.byref(vl)))
+        base = self.buf.data_ptr()
+
+        def view(p, nbytes, dt):
+            off = p.value - base
+            return self.buf[off:off + nbytes].view(dt).cpu().numpy()
+        return (view(rp, (self.n + 1) * 4, torch.int32).astype(np.int64) & 0xFFFFFFFF,
+                view(cl, self.nnz * 4, torch.int32).astype(np.int64) & 0xFFFFFFFF, view(vl, self.nnz * 8, torch.float64))
+
+    def relax(self, f, u, out=None, stream=None):
+        if out is None:
+            out = self.torch.empty_like(u)
+        _amg_check(lib().gf_amg_relax(self.h, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()),
+                                      C.c_void_p(out.data_ptr()), _stream_ptr(self.torch, stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().gf_amg_matrix_free(self.h)
             self.h = C.c_void_p()
 
     def __del__(self):

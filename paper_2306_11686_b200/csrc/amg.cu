@@ -1,0 +1,187 @@
+// amg.cu -- NEXT-4: the AMGmk relax kernel on sm_100a (include/gf_amg.h; readings R-AMG-MAT /
+// R-AMG-RELAX).  Independent of oracle/.
+//
+// Matrix build: every row's offset has a closed form -- the entries per row are cx(x) cy(y) cz(z)
+// (2 at a face, 3 inside, 1 on a length-1 axis), so the prefix over the rows before (x, y, z) is
+// Px(x) Sy Sz-planes etc. -- and each thread writes its row without atomics or scans.
+// Relax: kLanes lanes per row; lane q loads entries q+1, q+1+kLanes, ... of the row (coalesced
+// column / value loads, independent u gathers in flight), and the group subtracts the products in
+// row order through shuffles (the reading's left-to-right sum).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <new>
+#include <string>
+
+#include "gf_amg.h"
+
+namespace gfamg {
+
+constexpr int kTpb = 256;
+#ifndef GF_AMG_LANES
+#define GF_AMG_LANES 4
+#endif
+constexpr int kLanes = GF_AMG_LANES;
+
+__host__ __device__ inline long long axis_count(long long k, long long m) {
+  return m == 1 ? 1 : ((k == 0 || k == m - 1) ? 2 : 3);
+}
+// sum of axis_count over k' < k
+__host__ __device__ inline long long axis_prefix(long long k, long long m) {
+  if (m == 1) return k;  // (k is 0 or 1)
+  return k == 0 ? 0 : 2 + 3 * (k - 1) - (k == m ? 1 : 0);  // k == m: the last cell counts 2
+}
+
+__host__ __device__ inline long long row_offset(long long x, long long y, long long z, long long nx, long long ny,
+                                                long long nz) {
+  const long long Sx = axis_prefix(nx, nx), Sy = axis_prefix(ny, ny);
+  return axis_prefix(z, nz) * Sx * Sy + axis_count(z, nz) * (axis_prefix(y, ny) * Sx + axis_count(y, ny) * axis_prefix(x, nx));
+}
+
+__global__ void __launch_bounds__(kTpb) amg_build(int nx, int ny, int nz, uint32_t *__restrict__ rowptr,
+                                                  uint32_t *__restrict__ col, double *__restrict__ val) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)nx * ny * nz;
+  if (i >= n) return;
+  const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long long)nx * ny));
+  long long e = row_offset(x, y, z, nx, ny, nz);
+  rowptr[i] = (uint32_t)e;
+  if (i == n - 1) rowptr[n] = (uint32_t)(e + axis_count(x, nx) * axis_count(y, ny) * axis_count(z, nz));
+  col[e] = (uint32_t)i;
+  val[e++] = 26.0;
+  for (int dz = -1; dz <= 1; dz++)
+    for (int dy = -1; dy <= 1; dy++)
+      for (int dx = -1; dx <= 1; dx++) {
+        if (!dx && !dy && !dz) continue;
+        const int X = x + dx, Y = y + dy, Z = z + dz;
+        if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
+          col[e] = (uint32_t)(X + (long long)nx * (Y + (long long)ny * Z));
+          val[e++] = -1.0;
+        }
+      }
+}
+
+__global__ void __launch_bounds__(kTpb) amg_relax(uint32_t n, const uint32_t *__restrict__ rowptr,
+                                                  const uint32_t *__restrict__ col, const double *__restrict__ val,
+                                                  const double *__restrict__ f, const double *__restrict__ u,
+                                                  double *__restrict__ out) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t i = t / kLanes;
+  const int q = (int)(t % kLanes);
+  const bool live = i < n;
+  const uint32_t a = live ? __ldg(rowptr + i) : 0u, b = live ? __ldg(rowptr + i + 1) : 0u;
+  const unsigned gmask = (unsigned)((1ull << kLanes) - 1) << ((threadIdx.x & 31) & ~(kLanes - 1));
+  double res = live ? __ldg(f + i) : 0.0;
+  for (uint32_t e0 = a + 1; e0 < b; e0 += kLanes) {  // (a is the diagonal)
+    const uint32_t e = e0 + q;
+    const double p = e < b ? __dmul_rn(__ldg(val + e), __ldg(u + __ldg(col + e))) : 0.0;
+#pragma unroll
+    for (int k = 0; k < kLanes; k++) {
+      const double y = __shfl_sync(gmask, p, k, kLanes);
+      if (e0 + k < b) res = __dsub_rn(res, y);
+    }
+  }
+  if (live && q == 0) out[i] = __ddiv_rn(res, __ldg(val + a));
+}
+
+thread_local std::string t_err;
+gf_amg_status fail(gf_amg_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return s;
+}
+inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace gfamg
+
+using namespace gfamg;
+
+struct gf_amg_matrix {
+  int device;
+  uint32_t n, nnz;
+  const uint32_t *rowptr, *col;
+  const double *val;
+};
+
+extern "C" {
+
+const char *gf_amg_last_error(void) { return t_err.c_str(); }
+
+gf_amg_status gf_amg_matrix_bytes(int32_t nx, int32_t ny, int32_t nz, size_t *bytes, int64_t *nnz) {
+  if (!bytes || !nnz) return fail(GF_AMG_E_INVAL, "NULL output");
+  if (nx < 1 || ny < 1 || nz < 1) return fail(GF_AMG_E_INVAL, "grid %d x %d x %d", nx, ny, nz);
+  const long long n = (long long)nx * ny * nz;
+  if (n >= (1ll << 27)) return fail(GF_AMG_E_INVAL, "n = %lld >= 2^27", n);
+  const long long z = axis_prefix(nx, nx) * axis_prefix(ny, ny) * axis_prefix(nz, nz);
+  *nnz = z;
+  *bytes = al((n + 1) * 4) + al(z * 4) + al(z * 8);
+  return GF_AMG_OK;
+}
+
+gf_amg_status gf_amg_matrix_init(int32_t nx, int32_t ny, int32_t nz, int device, void *mem, size_t bytes,
+                                 gf_amg_stream_t stream, gf_amg_matrix **out) {
+  size_t need = 0;
+  int64_t nnz = 0;
+  gf_amg_status st = gf_amg_matrix_bytes(nx, ny, nz, &need, &nnz);
+  if (st != GF_AMG_OK) return st;
+  if (!mem || !out) return fail(GF_AMG_E_INVAL, "NULL argument");
+  if (bytes < need) return fail(GF_AMG_E_NOMEM, "buffer %zu B < %zu B", bytes, need);
+  if ((uintptr_t)mem & 255) return fail(GF_AMG_E_INVAL, "buffer must be 256-B aligned");
+  const long long n = (long long)nx * ny * nz;
+  char *m = static_cast<char *>(mem);
+  uint32_t *rowptr = reinterpret_cast<uint32_t *>(m);
+  uint32_t *col = reinterpret_cast<uint32_t *>(m + al((n + 1) * 4));
+  double *val = reinterpret_cast<double *>(m + al((n + 1) * 4) + al(nnz * 4));
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(GF_AMG_E_CUDA, "cannot make device %d current", device);
+  amg_build<<<(unsigned)((n + kTpb - 1) / kTpb), kTpb, 0, reinterpret_cast<cudaStream_t>(stream)>>>(nx, ny, nz, rowptr,
+                                                                                                    col, val);
+  const cudaError_t ce = cudaGetLastError();
+  cudaSetDevice(cur);
+  if (ce != cudaSuccess) return fail(GF_AMG_E_CUDA, "matrix build: %s", cudaGetErrorString(ce));
+  gf_amg_matrix *A = new (std::nothrow) gf_amg_matrix{device, (uint32_t)n, (uint32_t)nnz, rowptr, col, val};
+  if (!A) return fail(GF_AMG_E_NOMEM, "host allocation failed");
+  *out = A;
+  return GF_AMG_OK;
+}
+
+gf_amg_status gf_amg_matrix_free(gf_amg_matrix *A) {
+  delete A;
+  return GF_AMG_OK;
+}
+
+gf_amg_status gf_amg_matrix_info(const gf_amg_matrix *A, int64_t *n, int64_t *nnz, const uint32_t **rowptr,
+                                 const uint32_t **col, const double **val) {
+  if (!A) return fail(GF_AMG_E_INVAL, "matrix is NULL");
+  if (n) *n = A->n;
+  if (nnz) *nnz = A->nnz;
+  if (rowptr) *rowptr = A->rowptr;
+  if (col) *col = A->col;
+  if (val) *val = A->val;
+  return GF_AMG_OK;
+}
+
+gf_amg_status gf_amg_relax(const gf_amg_matrix *A, const double *d_f, const double *d_u, double *d_out,
+                           gf_amg_stream_t stream) {
+  if (!A || !d_f || !d_u || !d_out) return fail(GF_AMG_E_INVAL, "NULL argument");
+  if (d_u == d_out) return fail(GF_AMG_E_INVAL, "d_u and d_out alias (Jacobi sweep)");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(A->device) != cudaSuccess) return fail(GF_AMG_E_CUDA, "cannot make device current");
+  const long long threads = (long long)A->n * kLanes;
+  amg_relax<<<(unsigned)((threads + kTpb - 1) / kTpb), kTpb, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      A->n, A->rowptr, A->col, A->val, d_f, d_u, d_out);
+  const cudaError_t ce = cudaGetLastError();
+  cudaSetDevice(cur);
+  if (ce != cudaSuccess) return fail(GF_AMG_E_CUDA, "relax launch: %s", cudaGetErrorString(ce));
+  return GF_AMG_OK;
+}
+
+}  // extern "C"

@@ -223,3 +223,25 @@ def test_pagerank_abi_exports_and_checks():
     assert L.gf_pr_graph_bytes(100, 33, C.byref(gb), C.byref(sb)) == 1
     assert L.gf_pr_propagate(None, None, None, None, None) == 1
     assert L.gf_pr_last_error()
+
+
+def test_amg_abi_exports_and_checks():
+    """include/gf_amg.h (NEXT-4): exports, the closed-form nonzero count, argument checks."""
+    import os as _os
+    src = open(_os.path.join(_os.path.dirname(HEADER), "gf_amg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(gf_amg_\w+)\s*\(", src)))
+    assert len(names) == 6
+    out = subprocess.run(["nm", "-D", "--defined-only", gfbuild.LIB], capture_output=True, text=True).stdout
+    assert set(names) <= set(re.findall(r"\bT (gf_amg_\w+)", out))
+    import oracle as O
+    L = gf.lib()
+    b, nnz = C.c_size_t(), C.c_int64()
+    for dims in ((5, 4, 3), (1, 1, 1), (1, 7, 2), (64, 64, 64)):
+        assert L.gf_amg_matrix_bytes(*dims, C.byref(b), C.byref(nnz)) == 0
+        if dims[0] * dims[1] * dims[2] < 10000:
+            assert nnz.value == len(O.amg_matrix(*dims)[1])
+    assert nnz.value == 64 ** 3 * 27 - 6 * 64 * 64 * 9 + 12 * 64 * 3 - 8  # inclusion-exclusion, 27-point stencil
+    assert L.gf_amg_matrix_bytes(0, 4, 4, C.byref(b), C.byref(nnz)) == 1
+    assert L.gf_amg_relax(None, None, None, None, None) == 1
+    assert L.gf_amg_last_error()

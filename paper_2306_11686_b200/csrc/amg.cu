@@ -21,9 +21,13 @@ namespace gfamg {
 
 constexpr int kTpb = 256;
 #ifndef GF_AMG_LANES
-#define GF_AMG_LANES 4
+#define GF_AMG_LANES 2
 #endif
 constexpr int kLanes = GF_AMG_LANES;
+#ifndef GF_AMG_UNR
+#define GF_AMG_UNR 4
+#endif
+constexpr int kUnr = GF_AMG_UNR;  // row-loop unroll (loads of several rounds in flight)
 
 __host__ __device__ inline long long axis_count(long long k, long long m) {
   return m == 1 ? 1 : ((k == 0 || k == m - 1) ? 2 : 3);
@@ -72,18 +76,67 @@ __global__ void __launch_bounds__(kTpb) amg_relax(uint32_t n, const uint32_t *__
   const int q = (int)(t % kLanes);
   const bool live = i < n;
   const uint32_t a = live ? __ldg(rowptr + i) : 0u, b = live ? __ldg(rowptr + i + 1) : 0u;
-  const unsigned gmask = (unsigned)((1ull << kLanes) - 1) << ((threadIdx.x & 31) & ~(kLanes - 1));
+  // warp-uniform trip count (the longest row of the warp): the shuffles then run converged on the full
+  // mask (a per-group mask and trip count make the compiler re-check convergence with MATCH/VOTE every
+  // round, which saturated the ADU pipe: DESIGN.md Sec. 7)
+  const uint32_t len = __reduce_max_sync(0xffffffffu, b - a);
   double res = live ? __ldg(f + i) : 0.0;
-  for (uint32_t e0 = a + 1; e0 < b; e0 += kLanes) {  // (a is the diagonal)
-    const uint32_t e = e0 + q;
+#pragma unroll kUnr
+  for (uint32_t j = 1; j < len; j += kLanes) {  // (entry a is the diagonal)
+    const uint32_t e = a + j + q;
     const double p = e < b ? __dmul_rn(__ldg(val + e), __ldg(u + __ldg(col + e))) : 0.0;
+    if (kLanes == 1) {
+      res = __dsub_rn(res, p);
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < kLanes; k++) {
-      const double y = __shfl_sync(gmask, p, k, kLanes);
-      if (e0 + k < b) res = __dsub_rn(res, y);
+      const double y = __shfl_sync(0xffffffffu, p, k, kLanes);
+      if (a + j + k < b) res = __dsub_rn(res, y);
     }
   }
   if (live && q == 0) out[i] = __ddiv_rn(res, __ldg(val + a));
+}
+
+// CSR-stream variant (GF_AMG_STREAM=1): a CTA owns kRows consecutive rows; its threads first form
+// every product val[e] u[col[e]] of the CTA's contiguous nonzero range with fully coalesced loads into
+// shared memory, then each thread subtracts its row's products in order (same operations, same order).
+#ifndef GF_AMG_STREAM
+#define GF_AMG_STREAM 0
+#endif
+#ifndef GF_AMG_SU
+#define GF_AMG_SU 4
+#endif
+constexpr int kSU = GF_AMG_SU;  // products in flight per thread
+constexpr int kRows = 128;
+constexpr int kMaxRow = 27;
+__global__ void __launch_bounds__(kRows) amg_relax_stream(uint32_t n, const uint32_t *__restrict__ rowptr,
+                                                         const uint32_t *__restrict__ col,
+                                                         const double *__restrict__ val,
+                                                         const double *__restrict__ f, const double *__restrict__ u,
+                                                         double *__restrict__ out) {
+  __shared__ double prod[kRows * kMaxRow];
+  const uint32_t r0 = blockIdx.x * kRows;
+  const uint32_t r1 = min(n, r0 + kRows);
+  const uint32_t base = __ldg(rowptr + r0), end = __ldg(rowptr + r1);
+  const uint32_t cnt = end - base;
+  uint32_t k = threadIdx.x;
+  for (; k + (kSU - 1) * kRows < cnt; k += kSU * kRows) {
+    uint32_t c[kSU];
+    double v[kSU];
+#pragma unroll
+    for (int j = 0; j < kSU; j++) c[j] = __ldg(col + base + k + j * kRows), v[j] = __ldg(val + base + k + j * kRows);
+#pragma unroll
+    for (int j = 0; j < kSU; j++) prod[k + j * kRows] = __dmul_rn(v[j], __ldg(u + c[j]));
+  }
+  for (; k < cnt; k += kRows) prod[k] = __dmul_rn(__ldg(val + base + k), __ldg(u + __ldg(col + base + k)));
+  __syncthreads();
+  const uint32_t i = r0 + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t a = __ldg(rowptr + i) - base, b = __ldg(rowptr + i + 1) - base;
+  double res = __ldg(f + i);
+  for (uint32_t e = a + 1; e < b; e++) res = __dsub_rn(res, prod[e]);
+  out[i] = __ddiv_rn(res, __ldg(val + base + a));
 }
 
 thread_local std::string t_err;
@@ -175,9 +228,14 @@ gf_amg_status gf_amg_relax(const gf_amg_matrix *A, const double *d_f, const doub
   int cur = 0;
   cudaGetDevice(&cur);
   if (cudaSetDevice(A->device) != cudaSuccess) return fail(GF_AMG_E_CUDA, "cannot make device current");
+#if GF_AMG_STREAM
+  amg_relax_stream<<<(A->n + kRows - 1) / kRows, kRows, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      A->n, A->rowptr, A->col, A->val, d_f, d_u, d_out);
+#else
   const long long threads = (long long)A->n * kLanes;
   amg_relax<<<(unsigned)((threads + kTpb - 1) / kTpb), kTpb, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       A->n, A->rowptr, A->col, A->val, d_f, d_u, d_out);
+#endif
   const cudaError_t ce = cudaGetLastError();
   cudaSetDevice(cur);
   if (ce != cudaSuccess) return fail(GF_AMG_E_CUDA, "relax launch: %s", cudaGetErrorString(ce));

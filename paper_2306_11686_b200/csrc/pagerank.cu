@@ -164,6 +164,13 @@ __global__ void __launch_bounds__(kPrTpb) pr_contrib(uint32_t n, const double *_
 #define GF_PR_G 4
 #endif
 constexpr int kG = GF_PR_G;  // lanes per destination row
+#ifndef GF_PR_UNI
+#define GF_PR_UNI 1
+#endif
+#ifndef GF_PR_UNR
+#define GF_PR_UNR 4
+#endif
+constexpr int kPrUnr = GF_PR_UNR;
 
 __global__ void __launch_bounds__(kPrTpb) pr_gather(uint32_t n, const uint32_t *__restrict__ rowptr,
                                                     const uint32_t *__restrict__ col, const double *__restrict__ c,
@@ -173,8 +180,23 @@ __global__ void __launch_bounds__(kPrTpb) pr_gather(uint32_t n, const uint32_t *
   const int q = (int)(t % kG);
   const bool live = v < n;
   const uint32_t a = live ? __ldg(rowptr + v) : 0u, b = live ? __ldg(rowptr + v + 1) : 0u;
-  const unsigned gmask = (unsigned)((1ull << kG) - 1) << ((threadIdx.x & 31) & ~(kG - 1));  // this row's lanes
   double s = 0.0;
+#if GF_PR_UNI
+  // warp-uniform trip count (the warp's longest row): converged full-mask shuffles, no per-round
+  // convergence checks (MATCH/VOTE) from a per-group mask
+  const uint32_t len = __reduce_max_sync(0xffffffffu, b - a);
+#pragma unroll kPrUnr
+  for (uint32_t j = 0; j < len; j += kG) {
+    const uint32_t e = a + j + q;
+    const double x = e < b ? __ldg(c + __ldg(col + e)) : 0.0;
+#pragma unroll
+    for (int k = 0; k < kG; k++) {
+      const double y = __shfl_sync(0xffffffffu, x, k, kG);
+      if (a + j + k < b) s = __dadd_rn(s, y);  // every lane keeps the same running sum
+    }
+  }
+#else
+  const unsigned gmask = (unsigned)((1ull << kG) - 1) << ((threadIdx.x & 31) & ~(kG - 1));  // this row's lanes
   // rounds of kG edges: every lane fetches its edge of the round, then the group adds them in order
   for (uint32_t e0 = a; e0 < b; e0 += kG) {
     const uint32_t e = e0 + q;
@@ -185,6 +207,7 @@ __global__ void __launch_bounds__(kPrTpb) pr_gather(uint32_t n, const uint32_t *
       if (e0 + k < b) s = __dadd_rn(s, y);  // every lane keeps the same running sum
     }
   }
+#endif
   if (live && q == 0) {
     const double base = __ddiv_rn(__dsub_rn(1.0, 0.85), (double)n);
     out[v] = __dadd_rn(base, __dmul_rn(0.85, s));

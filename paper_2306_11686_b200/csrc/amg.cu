@@ -139,6 +139,45 @@ __global__ void __launch_bounds__(kRows) amg_relax_stream(uint32_t n, const uint
   out[i] = __ddiv_rn(res, __ldg(val + base + a));
 }
 
+// Warp-stream variant (GF_AMG_STREAM=2): a warp owns 32 consecutive rows, one per lane.  Phase 1: the
+// warp walks the rows' contiguous nonzero range 32 entries at a time (one line of col, two of val per
+// load instruction) and stages every product val[e] u[col[e]] in its own SMEM slice; phase 2: each lane
+// subtracts its row's products in order.  Same operations in the same order as amg_relax; no CTA sync.
+constexpr int kWarpsW = 4;
+__global__ void __launch_bounds__(32 * kWarpsW) amg_relax_warp(uint32_t n, const uint32_t *__restrict__ rowptr,
+                                                              const uint32_t *__restrict__ col,
+                                                              const double *__restrict__ val,
+                                                              const double *__restrict__ f,
+                                                              const double *__restrict__ u,
+                                                              double *__restrict__ out) {
+  __shared__ double prod[kWarpsW][32 * kMaxRow];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t r0 = (blockIdx.x * kWarpsW + w) * 32u;
+  if (r0 >= n) return;  // (warp-uniform)
+  const uint32_t r1 = min(n, r0 + 32u);
+  const uint32_t base = __ldg(rowptr + r0), cnt = __ldg(rowptr + r1) - base;
+  double *pw = prod[w];
+  const uint32_t *cb = col + base;
+  const double *vb = val + base;
+  uint32_t k = lane;
+  for (; k + 32 * (kSU - 1) < cnt; k += 32 * kSU) {
+    uint32_t c[kSU];
+    double v[kSU];
+#pragma unroll
+    for (int j = 0; j < kSU; j++) c[j] = __ldg(cb + k + 32 * j), v[j] = __ldg(vb + k + 32 * j);
+#pragma unroll
+    for (int j = 0; j < kSU; j++) pw[k + 32 * j] = __dmul_rn(v[j], __ldg(u + c[j]));
+  }
+  for (; k < cnt; k += 32) pw[k] = __dmul_rn(__ldg(vb + k), __ldg(u + __ldg(cb + k)));
+  __syncwarp();
+  const uint32_t i = r0 + lane;
+  if (i >= n) return;
+  const uint32_t a = __ldg(rowptr + i) - base, b = __ldg(rowptr + i + 1) - base;
+  double res = __ldg(f + i);
+  for (uint32_t e = a + 1; e < b; e++) res = __dsub_rn(res, pw[e]);
+  out[i] = __ddiv_rn(res, __ldg(vb + a));
+}
+
 thread_local std::string t_err;
 gf_amg_status fail(gf_amg_status s, const char *fmt, ...) {
   char buf[512];
@@ -228,7 +267,10 @@ gf_amg_status gf_amg_relax(const gf_amg_matrix *A, const double *d_f, const doub
   int cur = 0;
   cudaGetDevice(&cur);
   if (cudaSetDevice(A->device) != cudaSuccess) return fail(GF_AMG_E_CUDA, "cannot make device current");
-#if GF_AMG_STREAM
+#if GF_AMG_STREAM == 2
+  amg_relax_warp<<<(A->n + 32 * kWarpsW - 1) / (32 * kWarpsW), 32 * kWarpsW, 0,
+                   reinterpret_cast<cudaStream_t>(stream)>>>(A->n, A->rowptr, A->col, A->val, d_f, d_u, d_out);
+#elif GF_AMG_STREAM
   amg_relax_stream<<<(A->n + kRows - 1) / kRows, kRows, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       A->n, A->rowptr, A->col, A->val, d_f, d_u, d_out);
 #else

@@ -38,3 +38,24 @@ def test_matrix_and_sweeps_bit_exact(gf, dims):
         want = O.amg_relax(orp, ocol, oval, f, want)
         assert np.array_equal(dv.cpu().numpy(), want)
         du, dv = dv, du
+
+
+def test_bench_size_sweep_bit_exact(gf):
+    """A1's full size (256^3, 449 M nonzeros) in the launch configuration bench.py times: the whole
+    device matrix and one sweep compared element by element with the oracle (needs ~12 GB host RAM)."""
+    import psutil
+    import torch
+    if psutil.virtual_memory().available < 24 << 30:
+        pytest.skip("needs ~24 GB free host memory for the oracle's 256^3 matrix")
+    A = gf.AMGMatrix(256, 256, 256)
+    orp, ocol, oval = O.amg_matrix(256, 256, 256)
+    rp, col, val = A.arrays()
+    assert np.array_equal(rp, orp)
+    assert np.array_equal(col, ocol)
+    assert np.array_equal(val, oval)
+    del col, val
+    rng = np.random.default_rng(7)
+    f, u = rng.random(A.n), rng.random(A.n)
+    out = torch.empty(A.n, dtype=torch.float64, device="cuda")
+    A.relax(torch.from_numpy(f).cuda(), torch.from_numpy(u).cuda(), out)
+    assert np.array_equal(out.cpu().numpy(), O.amg_relax(orp, ocol, oval, f, u))

@@ -456,8 +456,13 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 // Scratch of one lookup slot.  Device-resident calls use one slot sized for the whole batch.  Host-IO
 // calls (GF_HOST_IO) are pipelined in chunks of kIoChunk lookups over two slots and three streams:
 // chunk c's host->device copy, chunk c-1's lookup and chunk c-2's device->host copy overlap (PCIe is
-// full duplex).  Each chunk is sorted and looked up on its own; results are identical.
-constexpr uint64_t kIoChunk = 1ull << 21;
+// full duplex).  Each chunk is sorted and looked up on its own; results are identical.  4 M-lookup
+// chunks (C3 e2e, hash only: 2^21 2.0e9, 2^22 2.37e9, 2^23 2.47e9 lookups/s; with the macro output
+// 1.18 / 1.10 / 0.99e9): a chunk at or above the group kernel's 4 M threshold.
+#ifndef GF_IO_CHUNK_LOG2
+#define GF_IO_CHUNK_LOG2 22
+#endif
+constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
   size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, h_macro, h_E, h_mat, bytes;

@@ -114,6 +114,8 @@ gf_status gf_xs_grid_free(gf_xs_grid *g);
  *   GF_ARR_HASH_GRID     uint16 [n_iso][pitch]    nuclide-major HG, pitch >= hash_bins
  *   GF_ARR_UNION_BINS    uint32 [2^20 + 1]        #{U < b / 2^20}: top level of the unionized search
  *   GF_ARR_RECIP_WIDTH   double [n_iso][n_gp]     RN(1 / (E[k+1] - E[k])) per interval (exact division)
+ *   GF_ARR_NUCLIDE_BINS  uint16 [n_iso][pitch]    unionized whole grids with n_gp < 65536: #{E_nuc <= b / 2^14},
+ *                                                 b = 0..2^14 -- the sparse-batch search (history waves)
  *   GF_ARR_INTERVALS     double [n_iso][n_gp][16] unionized / hash grids: per interval k < n_gp-1 the
  *                        sorted kernel's 128-B record E[k+1], E[k+1]-E[k], (xs_c[k+1], xs_c[k+1]-xs_c[k])
  *                        for c = 0..4, RN(1/(E[k+1]-E[k])), E[k], 0, 0 (all RN); record n_gp-1 is zero
@@ -132,7 +134,7 @@ typedef enum {
     GF_ARR_CONCS = 5, GF_ARR_MAT_NUCS = 6, GF_ARR_MAT_OFFSETS = 7, GF_ARR_THRESHOLDS = 8,
     GF_ARR_RS_POLES = 9, GF_ARR_RS_POLE_L = 10, GF_ARR_RS_WINDOWS = 11, GF_ARR_RS_K0RS = 12,
     GF_ARR_RS_POLE_OFF = 13, GF_ARR_RS_WIN_OFF = 14, GF_ARR_UNION_BINS = 15,
-    GF_ARR_RECIP_WIDTH = 16, GF_ARR_INTERVALS = 17
+    GF_ARR_RECIP_WIDTH = 16, GF_ARR_INTERVALS = 17, GF_ARR_NUCLIDE_BINS = 18
 } gf_array;
 gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr, size_t *bytes, int64_t *pitch_out);
 

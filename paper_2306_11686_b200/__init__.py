@@ -28,7 +28,7 @@ ABI_VERSION = 1
 
 ARR = dict(nuclide_grid=0, energy=1, unionized=2, index_grid=3, hash_grid=4, concs=5, mat_nucs=6, mat_offsets=7,
            thresholds=8, rs_poles=9, rs_pole_l=10, rs_windows=11, rs_K0RS=12, rs_pole_off=13, rs_win_off=14, union_bins=15,
-           recip_width=16, intervals=17)
+           recip_width=16, intervals=17, nuclide_bins=18)
 
 _STATUS = {0: "GF_OK", 1: "GF_E_INVAL", 2: "GF_E_NOMEM", 3: "GF_E_CUDA", 4: "GF_E_UNSUPPORTED", 5: "GF_E_MISMATCH"}
 
@@ -217,7 +217,7 @@ class Grid:
         off = p.value - self.buf.data_ptr()
         raw = self.buf[off:off + nb.value]
         dt = {"nuclide_grid": torch.float64, "energy": torch.float64, "unionized": torch.float64,
-              "index_grid": torch.int16, "hash_grid": torch.int16, "union_bins": torch.int32, "recip_width": torch.float64, "intervals": torch.float64, "concs": torch.float64, "mat_nucs": torch.int32,
+              "index_grid": torch.int16, "hash_grid": torch.int16, "union_bins": torch.int32, "recip_width": torch.float64, "intervals": torch.float64, "nuclide_bins": torch.int16, "concs": torch.float64, "mat_nucs": torch.int32,
               "mat_offsets": torch.int32, "thresholds": torch.float64, "rs_poles": torch.float64,
               "rs_pole_l": torch.int32, "rs_windows": torch.float64, "rs_K0RS": torch.float64,
               "rs_pole_off": torch.int32, "rs_win_off": torch.int32}[name]

@@ -102,7 +102,8 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   // XS
-  size_t G, Ed, Rd, XR, flags, U, IG, HG, ubin;
+  size_t G, Ed, Rd, XR, flags, U, IG, HG, ubin, NB;
+  int nb_pitch;
   size_t k0, binfo;  // NEXT-2 band grid: k0 / cnt / first [3][n_iso] u32, band info 16 B
   int band_cap;      // in-band points per nuclide the layout holds
   long long ig_pitch;
@@ -180,6 +181,10 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
       L.U = take(nu * 8);
       L.IG = take((size_t)p->n_isotopes * (size_t)L.ig_pitch * 2);
       L.ubin = take((size_t)(kUBins + 1) * 4);
+      if (p->n_bands <= 1 && p->n_gridpoints < 65536) {
+        L.nb_pitch = ((1 << kNbLog2) + 1 + 63) & ~63;
+        L.NB = take((size_t)p->n_isotopes * L.nb_pitch * 2);
+      }
       L.scratch_bytes = al(npts * 8);
       if (p->n_bands > 1) {
         L.k0 = take((size_t)p->n_isotopes * 12);
@@ -366,6 +371,10 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
       uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
       X.G = G; X.Ed = Ed; X.Rd = Rd; X.XR = XR; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
+      uint16_t *NB = (X.grid_type == GF_GRID_UNIONIZED && L.nb_pitch) ? reinterpret_cast<uint16_t *>(base + L.NB)
+                                                                       : nullptr;
+      X.NB = NB;
+      X.nb_pitch = L.nb_pitch;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
       const bool banded = X.grid_type == GF_GRID_UNIONIZED && p->n_bands > 1;
       X.k0 = banded ? reinterpret_cast<uint32_t *>(base + L.k0) : nullptr;
@@ -380,6 +389,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       if (ubin) put(GF_ARR_UNION_BINS, ubin, (size_t)(kUBins + 1) * 4, kUBins + 1);
       put(GF_ARR_RECIP_WIDTH, Rd, npts * 8, X.n_gp);
       if (XR) put(GF_ARR_INTERVALS, XR, npts * 128, X.n_gp);
+      if (NB) put(GF_ARR_NUCLIDE_BINS, NB, (size_t)X.n_iso * X.nb_pitch * 2, X.nb_pitch);
       ce = launch_xs_grid(X, G, Ed, Rd, XR, zero_width, U, IG, HG, ubin, mconc, p->init_seed,
                           static_cast<double *>(scratch), st);
       if (ce == cudaSuccess && banded) {  // NEXT-2: the band's U (sync: its length sizes the index grid)
@@ -397,6 +407,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
         X.n_union = (long long)info[0] + 2;
         if (ce == cudaSuccess) ce = launch_band_index(X, U, IG, ubin, st);
       }
+      if (ce == cudaSuccess && NB) ce = launch_nb_build(X, NB, st);
       if (U) put(GF_ARR_UNIONIZED, U, (size_t)X.n_union * 8, (int64_t)X.n_union);
       // the exact reciprocal division is used only if no interval has zero (or underflowing) width
       int zw = 1;

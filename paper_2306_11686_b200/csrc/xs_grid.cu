@@ -326,6 +326,28 @@ __global__ void __launch_bounds__(256) ig_build(const double *__restrict__ Ed, c
   for (int k = 0; k < 4; k++) dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
 }
 
+// Per-nuclide bin counts of the sparse-batch search: NB[nuc][b] = #{E_nuc[j] <= b 2^-kNbLog2}
+// (exact edges; a bisection over the sorted energies).  For E in [b, b+1) 2^-kNbLog2 the count
+// #{E_nuc <= E} lies in [NB[b], NB[b+1]].
+__global__ void nb_build(const double *__restrict__ Ed, uint16_t *__restrict__ NB, int n_gp, int pitch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x, nuc = blockIdx.y;
+  if (b > (1 << kNbLog2)) return;
+  const double e = ldexp((double)b, -kNbLog2);
+  const double *A = Ed + (size_t)nuc * n_gp;
+  int lo = 0, hi = n_gp;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] <= e) lo = mid + 1; else hi = mid;
+  }
+  NB[(size_t)nuc * pitch + b] = (uint16_t)lo;
+}
+
+cudaError_t launch_nb_build(const XsDev &X, uint16_t *NB, cudaStream_t st) {
+  dim3 grid(((1 << kNbLog2) + 1 + 255) / 256, X.n_iso);
+  nb_build<<<grid, 256, 0, st>>>(X.Ed, NB, X.n_gp, X.nb_pitch);
+  return cudaGetLastError();
+}
+
 // Top-level table of the two-level unionized search: ubin[b] = #{U < b / 2^20}, ubin[2^20] = n.
 __global__ void ubin_build(const double *__restrict__ U, uint32_t *__restrict__ ubin, long long n_union) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;

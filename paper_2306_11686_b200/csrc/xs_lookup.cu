@@ -47,6 +47,11 @@ __device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
     long long u = lo - 1;
     u = u < 0 ? 0 : u;
     return u > X.n_union - 2 ? X.n_union - 2 : u;
+  } else if (GT == kGridNB) {
+    // bin b = floor(E 2^kNbLog2) of the per-nuclide tables for E in [0, 1); otherwise -(u + 1) with u
+    // the unionized index (the interval then comes from the index grid)
+    if (E >= 0.0 && E < 1.0) return (long long)__dmul_rn(E, (double)(1 << kNbLog2));
+    return -1 - energy_index<GF_GRID_UNIONIZED>(X, E);
   } else if (GT == GF_GRID_HASH) {
     const double du = __ddiv_rn(1.0, (double)X.bins);
     long long b = (long long)__ddiv_rn(E, du);  // truncation toward zero, as the C cast
@@ -69,14 +74,16 @@ struct XsTables {
 
 // PK: the group kernel's packed layout, one 16-B entry {nuc * n_gp, nuc * pitch, conc} (ent and conc
 // stay unset); otherwise the separate ent / conc arrays.
-template <bool PK = false>
+// NBP: the row base of entry j is nuc * nb_pitch (kGridNB kernels) instead of the index / hash grid's.
+template <bool PK = false, bool NBP = false>
 __device__ __forceinline__ XsTables stage_xs_tables(const XsDev &X, unsigned char *smem) {
   int32_t *s_off = reinterpret_cast<int32_t *>(smem);          // 16 ints
   double *s_thr = reinterpret_cast<double *>(smem + 64);       // 12 doubles -> 160
   double *s_conc = reinterpret_cast<double *>(smem + 160);     // total doubles
   uint2 *s_ent = reinterpret_cast<uint2 *>(smem + 160 + 8 * (size_t)X.total);
   uint4 *s_pk = reinterpret_cast<uint4 *>(smem + 160);         // PK: 16-B aligned (160 % 16 == 0)
-  const uint32_t pitch = (uint32_t)(X.grid_type == GF_GRID_UNIONIZED ? X.ig_pitch : X.hg_pitch);
+  const uint32_t pitch =
+      NBP ? (uint32_t)X.nb_pitch : (uint32_t)(X.grid_type == GF_GRID_UNIONIZED ? X.ig_pitch : X.hg_pitch);
   for (int t = threadIdx.x; t < X.total; t += blockDim.x) {
     const uint32_t nuc = (uint32_t)X.mnuc[t];
     const double c = X.mconc[t];
@@ -123,6 +130,23 @@ __device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, 
     k = bisect<int>(X.Ed + e.x, E, 0, n_gp - 1);
   } else if (GT == GF_GRID_UNIONIZED) {
     k = __ldg(X.IG + e.y + (uint32_t)idx);
+  } else if (GT == kGridNB) {
+    // sparse batches: #{E_nuc <= E} lies in [NB[b], NB[b+1]] (a 2^14-bin table per nuclide, L2-resident,
+    // ~0.7 points per bin), finished by a bisection over that bracket -- the same interval as the
+    // index grid's, without a DRAM sector of the index grid per (lookup, nuclide)
+    if (idx >= 0) {
+      const uint16_t *nb = X.NB + e.y + (uint32_t)idx;
+      int lo = __ldg(nb), hi = __ldg(nb + 1);
+      const double *A = X.Ed + e.x;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(A + mid) <= E) lo = mid + 1; else hi = mid;
+      }
+      k = lo > 0 ? lo - 1 : 0;
+    } else {
+      const uint32_t nuc = e.y / (uint32_t)X.nb_pitch;
+      k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + (uint32_t)(-idx - 1));
+    }
   } else {
     const double *Ed = X.Ed + e.x;
     int lo_, hi_;
@@ -262,14 +286,17 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
 
 // Lookups over the locality-sorted order: position p holds energy Es[p]; its material is the
 // segment of mstart that contains p; its original position is idx[p] (outputs only).
+#ifndef GF_SORTED_MINB
+#define GF_SORTED_MINB 6  // 80 registers, 6 CTAs per SM (H3 15.5 -> 15.0 ms, H2 4.55 -> 4.10 ms; 8: 300 B spills)
+#endif
 template <int GT>
-__global__ void __launch_bounds__(kLookupTpb) xs_lookup_sorted(XsDev X, uint32_t n, const double *__restrict__ Es,
+__global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(XsDev X, uint32_t n, const double *__restrict__ Es,
                                                                const uint32_t *__restrict__ idx,
                                                                const uint32_t *__restrict__ mstart,
                                                                OutSpec out,
                                                                unsigned long long *__restrict__ vsum) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const XsTables T = stage_xs_tables(X, smem);
+  const XsTables T = stage_xs_tables<false, GT == kGridNB>(X, smem);
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   n = min(n, __ldg(mstart + kMats));  // lookups kept by the sort (band grids keep their band's)
   uint32_t v = 0;
@@ -314,6 +341,13 @@ static int sorted_kernel(uint32_t n) {
   return n >= nmin ? kKernGroup : kKernThread;
 }
 
+// Sparse batches on a unionized grid (below kGroupMinN: history waves, host-IO chunks) search the
+// per-nuclide bin tables instead of the index grid; GF_XS_NB=0 in the environment disables it (A/B).
+static bool use_nb() {
+  const char *s = getenv("GF_XS_NB");
+  return !(s && s[0] == '0');
+}
+
 template <int GT>
 static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                              const uint8_t *src_mat, bool sort, const SortScratch &S, const OutSpec &out,
@@ -337,6 +371,12 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
       if ((e = allow_smem(xs_lookup_warp_nuclide, smem)) != cudaSuccess) return e;
       xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                            vsum);
+      return cudaGetLastError();
+    }
+    if (GT == GF_GRID_UNIONIZED && X.NB && use_nb()) {
+      if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;
+      xs_lookup_sorted<kGridNB><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
+                                                                               vsum);
       return cudaGetLastError();
     }
     if ((e = allow_smem(xs_lookup_sorted<GT>, smem)) != cudaSuccess) return e;

@@ -666,3 +666,36 @@ def test_argmax_robustness_report(gf, torch):
     gap_rs = ((s[:, -1] - s[:, -2]) / s[:, -1].abs()).min().item()
     print(f"min top-2 relative gap: XS C3 2M {gap_xs:.3e}, RS C5 500k {gap_rs:.3e}")
     assert gap_xs > 1e-12 and gap_rs > 1e-8
+
+
+def test_nuclide_bin_search_sparse_batches(gf, torch, monkeypatch):
+    """Sparse batches on a unionized grid (below the group kernel's 4 M threshold) search the
+    per-nuclide bin tables NB (#{E_nuc <= b 2^-14}) instead of the index grid.  The table is checked
+    against a plain count over the device's energy column, and the lookups -- at NB bin edges, their
+    ulp neighbours, exact gridpoints and outside [0, 1), where the kernel falls back to the index
+    grid -- against the oracle, with the NB search on and off."""
+    o, g = make_pair(gf, 68, 11303, 1)
+    nbt, pitch = g.array("nuclide_bins")
+    nb = nbt.cpu().numpy().astype(np.int64).reshape(68, pitch)
+    Ed = g.array("energy")[0].cpu().numpy().reshape(68, 11303)
+    edges = np.ldexp(np.arange(2 ** 14 + 1, dtype=np.float64), -14)
+    for nuc in (0, 1, 33, 67):
+        assert np.array_equal(nb[nuc, :2 ** 14 + 1], np.searchsorted(Ed[nuc], edges, side="right"))
+    rng = np.random.default_rng(14)
+    E, mats = edge_energies(o, 4000, 5)
+    extra = [-0.25, -5e-324, 1.0, 1.5, math.nextafter(1.0, 2)]
+    for b in list(rng.integers(1, 2 ** 14, 40)) + [1, 2 ** 14 - 1]:
+        e = float(b) * 2.0 ** -14
+        extra += [e, math.nextafter(e, 0), math.nextafter(e, 2)]
+    G = o.nuclide_grid()
+    for nuc in (2, 40):
+        for k in rng.integers(0, o.n_gp - 1, 20):
+            e = float(G[nuc, k, 0])
+            extra += [e, math.nextafter(e, 0), math.nextafter(e, 2)]
+    E = np.concatenate([E, np.array(extra)])
+    mats = np.concatenate([mats, rng.integers(0, 12, len(extra)).astype(np.uint8)])
+    raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
+    for flag in ("1", "0"):
+        monkeypatch.setenv("GF_XS_NB", flag)
+        raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
+        assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o), flag

@@ -48,10 +48,10 @@ __device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
     u = u < 0 ? 0 : u;
     return u > X.n_union - 2 ? X.n_union - 2 : u;
   } else if (GT == kGridNB) {
-    // bin b = floor(E 2^kNbLog2) of the per-nuclide tables for E in [0, 1); otherwise -(u + 1) with u
-    // the unionized index (the interval then comes from the index grid)
+    // bin b = floor(E 2^kNbLog2) of the per-nuclide tables for E in [0, 1); otherwise -1 (the interval
+    // then comes from the index grid)
     if (E >= 0.0 && E < 1.0) return (long long)__dmul_rn(E, (double)(1 << kNbLog2));
-    return -1 - energy_index<GF_GRID_UNIONIZED>(X, E);
+    return -1;
   } else if (GT == GF_GRID_HASH) {
     const double du = __ddiv_rn(1.0, (double)X.bins);
     long long b = (long long)__ddiv_rn(E, du);  // truncation toward zero, as the C cast
@@ -134,7 +134,7 @@ __device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, 
     // sparse batches: #{E_nuc <= E} lies in [NB[b], NB[b+1]] (a 2^14-bin table per nuclide, L2-resident,
     // ~0.7 points per bin), finished by a bisection over that bracket -- the same interval as the
     // index grid's, without a DRAM sector of the index grid per (lookup, nuclide)
-    if (idx >= 0) {
+    if ((unsigned long long)idx < (1ull << kNbLog2)) {  // (a u32 0xFFFFFFFF from idx_prep also fails it)
       const uint16_t *nb = X.NB + e.y + (uint32_t)idx;
       int lo = __ldg(nb), hi = __ldg(nb + 1);
       const double *A = X.Ed + e.x;
@@ -145,7 +145,7 @@ __device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, 
       k = lo > 0 ? lo - 1 : 0;
     } else {
       const uint32_t nuc = e.y / (uint32_t)X.nb_pitch;
-      k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + (uint32_t)(-idx - 1));
+      k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E));
     }
   } else {
     const double *Ed = X.Ed + e.x;

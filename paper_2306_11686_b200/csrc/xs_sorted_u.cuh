@@ -347,16 +347,13 @@ template <int GT, bool FAST>
 static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
                                 unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = xs_table_smem(X.total);
-  static int blocks_per_sm = 0;
-  static size_t smem_cfg = 0;
+  // set per call (the attribute is per device; no cached state shared between host threads)
+  int blocks_per_sm = 0;
   cudaError_t e;
-  if (smem_cfg != smem) {
-    if ((e = allow_smem(xs_lookup_group<GT, FAST>, smem)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_group<GT, FAST>, kTpbL, smem)) !=
-        cudaSuccess)
-      return e;
-    smem_cfg = smem;
-  }
+  if ((e = allow_smem(xs_lookup_group<GT, FAST>, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_group<GT, FAST>, kTpbL, smem)) !=
+      cudaSuccess)
+    return e;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -262,18 +262,15 @@ template <bool FAST>
 static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
                                  unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = staged_smem(X.total);
-  static int blocks_per_sm[2] = {0, 0};
-  static size_t smem_cfg[2] = {0, 0};
+  // set per call (the attribute is per device; no cached state shared between host threads)
+  int blocks_per_sm = 0;
   cudaError_t e;
-  if (smem_cfg[FAST] != smem) {
-    if ((e = cudaFuncSetAttribute(xs_lookup_staged<FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[FAST], xs_lookup_staged<FAST>,
-                                                           kStagedThreads, smem)) != cudaSuccess)
-      return e;
-    smem_cfg[FAST] = smem;
-  }
+  if ((e = cudaFuncSetAttribute(xs_lookup_staged<FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_staged<FAST>, kStagedThreads,
+                                                         smem)) != cudaSuccess)
+    return e;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -281,7 +278,7 @@ static cudaError_t launch_staged(const XsDev &X, uint32_t n, const SortScratch &
   TileInfo *tinfo = reinterpret_cast<TileInfo *>(S.tinfo);
   staged_prep<<<ntiles, kTile, 0, st>>>(X, n, S.Es, S.mstart, S.us, tinfo);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm[FAST], 1)));
+  const uint32_t grid = min(ntiles, (uint32_t)(sms * max(blocks_per_sm, 1)));
   xs_lookup_staged<FAST><<<grid, kStagedThreads, smem, st>>>(X, n, S.Es, S.us, tinfo, S.idx, S.mstart, out,
                                                              vsum);
   return cudaGetLastError();

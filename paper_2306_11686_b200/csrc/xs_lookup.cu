@@ -226,6 +226,70 @@ __device__ __forceinline__ void nuclide_loop(const XsDev &X, const XsTables &T, 
   }
 }
 
+// kGridNB with E in [0, 1) (bin b): a three-stage ring so that no step waits on a load issued in the
+// same step -- step j issues the NB bracket loads of nuclide j+3, the one probe Ed[lo] of nuclide j+2
+// (when its bracket holds one point: c = lo + (Ed[lo] <= E)), resolves the interval of j+1 and issues
+// its record pair, then accumulates j.  Brackets of two or more points (~15%) bisect at resolve time.
+// Same intervals as interval<kGridNB>; the accumulation order is unchanged.
+#ifndef GF_NB_RING
+#define GF_NB_RING 1
+#endif
+#ifndef GF_NB_RING_MIN
+#define GF_NB_RING_MIN 64  // materials with at least this many nuclides take the ring (the large fuel, 321)
+#endif
+__device__ __forceinline__ void nb_bracket(const XsDev &X, uint2 e, uint32_t b, int &lo, int &hi) {
+  const uint16_t *q = X.NB + e.y + b;
+  lo = __ldg(q);
+  hi = __ldg(q + 1);
+}
+__device__ __forceinline__ double nb_probe(const XsDev &X, uint2 e, int lo, int hi) {
+  return hi - lo == 1 ? __ldg(X.Ed + e.x + lo) : 0.0;
+}
+__device__ __forceinline__ uint32_t nb_resolve(const XsDev &X, uint2 e, double E, int lo, int hi, double pr) {
+  int c;
+  if (hi - lo <= 0) {
+    c = lo;
+  } else if (hi - lo == 1) {
+    c = lo + (pr <= E ? 1 : 0);
+  } else {
+    const double *A = X.Ed + e.x;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(A + mid) <= E) lo = mid + 1; else hi = mid;
+    }
+    c = lo;
+  }
+  const int k = c > 0 ? c - 1 : 0;
+  return (uint32_t)(k > X.n_gp - 2 ? X.n_gp - 2 : k);
+}
+
+template <bool FAST>
+__device__ __forceinline__ void nuclide_loop_nb(const XsDev &X, const XsTables &T, double E, uint32_t b, int j0,
+                                                int j1, double m[5]) {
+  int lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0, lo3 = 0, hi3 = 0;
+  double pr1 = 0.0, pr2 = 0.0;
+  Pair P, Q;
+  {
+    int lo0, hi0;
+    nb_bracket(X, T.ent[j0], b, lo0, hi0);
+    const double pr0 = nb_probe(X, T.ent[j0], lo0, hi0);
+    if (j0 + 1 < j1) nb_bracket(X, T.ent[j0 + 1], b, lo1, hi1);
+    if (j0 + 2 < j1) nb_bracket(X, T.ent[j0 + 2], b, lo2, hi2);
+    if (j0 + 1 < j1) pr1 = nb_probe(X, T.ent[j0 + 1], lo1, hi1);
+    load_pair<FAST>(X, T.ent[j0].x + nb_resolve(X, T.ent[j0], E, lo0, hi0, pr0), P);
+  }
+#pragma unroll 2
+  for (int j = j0; j < j1; j++) {
+    if (j + 3 < j1) nb_bracket(X, T.ent[j + 3], b, lo3, hi3);
+    if (j + 2 < j1) pr2 = nb_probe(X, T.ent[j + 2], lo2, hi2);
+    if (j + 1 < j1) load_pair<FAST>(X, T.ent[j + 1].x + nb_resolve(X, T.ent[j + 1], E, lo1, hi1, pr1), Q);
+    accumulate<FAST>(P, E, T.conc[j], m);
+    P = Q;
+    lo1 = lo2; hi1 = hi2; pr1 = pr2;
+    lo2 = lo3; hi2 = hi3;
+  }
+}
+
 template <int GT, bool PF>
 __device__ __forceinline__ void macro_xs(const XsDev &X, const XsTables &T, double E, long long idx, int mat,
                                          double m[5]) {
@@ -233,6 +297,13 @@ __device__ __forceinline__ void macro_xs(const XsDev &X, const XsTables &T, doub
   for (int c = 0; c < 5; c++) m[c] = 0.0;
   const int j0 = T.off[mat], j1 = T.off[mat + 1];
   if (j0 >= j1) return;
+  if (GT == kGridNB && GF_NB_RING && j1 - j0 >= GF_NB_RING_MIN && (unsigned long long)idx < (1ull << kNbLog2)) {
+    if (X.fastdiv)
+      nuclide_loop_nb<true>(X, T, E, (uint32_t)idx, j0, j1, m);
+    else
+      nuclide_loop_nb<false>(X, T, E, (uint32_t)idx, j0, j1, m);
+    return;
+  }
   // the reciprocal division needs |hi.E - E| <= 4 (all sampled energies are in [0, 1])
   if (X.fastdiv && fabs(E) <= 2.0)
     nuclide_loop<GT, true, PF>(X, T, E, idx, j0, j1, m);
@@ -287,7 +358,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
 // Lookups over the locality-sorted order: position p holds energy Es[p]; its material is the
 // segment of mstart that contains p; its original position is idx[p] (outputs only).
 #ifndef GF_SORTED_MINB
-#define GF_SORTED_MINB 6  // 80 registers, 6 CTAs per SM (H3 15.5 -> 15.0 ms, H2 4.55 -> 4.10 ms; 8: 300 B spills)
+#define GF_SORTED_MINB 5  // 5 CTAs per SM (with the NB ring: H3 14.2 -> 13.3 ms; 6 CTAs spill 176 B)
 #endif
 template <int GT>
 __global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(XsDev X, uint32_t n, const double *__restrict__ Es,

@@ -12,6 +12,8 @@
 // buckets per CTA run, then a per-bucket fine sort) moved fewer DRAM bytes but was not faster.
 #include "gf_internal.cuh"
 
+#include <cstdlib>
+
 namespace gf {
 
 #ifndef GF_DIAG_SCATTER
@@ -178,6 +180,10 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 // small ones so that the zeroing and the two scans over 12 x 2^b counters stay small next to the batch
 // (a 500 k-lookup history wave: 2^14), i.e. ~4 lookups per bin of the average material, b in [10, 17].
 static int sort_bits(uint32_t n) {
+  if (const char *f = getenv("GF_SORT_BITS")) {  // A/B override, clamped to the scratch layout's [10, 17]
+    const int v = atoi(f);
+    if (v >= 10 && v <= 17) return v;
+  }
   int b = 10;
   while (b < 17 && ((uint64_t)kMats << (b + 2)) < n) b++;
   return b;

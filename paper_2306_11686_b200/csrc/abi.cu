@@ -481,15 +481,34 @@ struct SlotLayout {
 struct BatchLayout {
   SlotLayout slot;
   int slots;
+  SlotLayout full;  // host-IO, sorted, energies, no per-lookup output: one whole-batch slot (counts overlap
+  bool has_full;    // the chunked H2D; one sort and one lookup pass over the whole batch), aliasing the slots
   size_t h_vsum, total;
 };
+
+static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want_macro, bool energies,
+                      SlotLayout &L);
 
 static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
                        BatchLayout &B) {
   memset(&B, 0, sizeof B);
   const bool host_io = (flags & GF_HOST_IO) != 0;
   const uint64_t m = host_io ? (n < kIoChunk ? n : kIoChunk) : n;
-  SlotLayout &L = B.slot;
+  plan_slot(g, m, flags, want_macro, energies, B.slot);
+  B.slots = host_io ? 2 : 1;
+  size_t end = B.slots * B.slot.bytes;
+  if (host_io && energies && (flags & GF_SORT_LOCALITY)) {
+    plan_slot(g, n, flags, false, true, B.full);
+    B.has_full = true;
+    end = std::max(end, B.full.bytes);
+  }
+  B.h_vsum = end;
+  B.total = B.h_vsum + (host_io ? 256 : 0);
+}
+
+static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want_macro, bool energies,
+                      SlotLayout &L) {
+  const bool host_io = (flags & GF_HOST_IO) != 0;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -515,9 +534,6 @@ static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool wan
     }
   }
   L.bytes = al(o > 0 ? o : 256);
-  B.slots = host_io ? 2 : 1;
-  B.h_vsum = B.slots * L.bytes;
-  B.total = B.h_vsum + (host_io ? 256 : 0);
 }
 
 gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes) {
@@ -574,6 +590,34 @@ static gf_status run_host_io(const gf_xs_grid *gc, uint64_t first, uint64_t n, u
   GF_CUDA(cudaStreamWaitEvent(sin, start, 0));
   GF_CUDA(cudaStreamWaitEvent(scomp, start, 0));
   GF_CUDA(cudaMemsetAsync(dvsum, 0, 8, scomp));
+  if (energies && sort && !macro_out && B.has_full) {
+    // whole-batch mode: the chunks' host->device copies overlap the counting pass of the locality sort;
+    // then one scatter and one lookup pass over the whole batch (full sort locality, the group kernel)
+    const SlotLayout &L = B.full;
+    SortScratch S = slot_sort(sc, L);
+    S.counted = true;
+    double *dE = reinterpret_cast<double *>(sc + L.h_E);
+    uint8_t *dmat = reinterpret_cast<uint8_t *>(sc + L.h_mat);
+    const double *thr = g->p.bench == GF_XSBENCH ? g->xs.thr : g->rs.thr;
+    cudaError_t ce = launch_sort_zero((uint32_t)n, S, scomp);
+    if (ce != cudaSuccess) return fail(GF_E_CUDA, "sort: %s", cudaGetErrorString(ce));
+    for (uint64_t off = 0; off < n; off += kIoChunk) {
+      const uint64_t cn = (n - off < kIoChunk) ? n - off : kIoChunk;
+      GF_CUDA(cudaMemcpyAsync(dE + off, E + off, sizeof(double) * cn, cudaMemcpyHostToDevice, sin));
+      GF_CUDA(cudaMemcpyAsync(dmat + off, mat + off, cn, cudaMemcpyHostToDevice, sin));
+      GF_CUDA(cudaEventRecord(h2d[0], sin));
+      GF_CUDA(cudaStreamWaitEvent(scomp, h2d[0], 0));
+      ce = launch_sort_count((uint32_t)n, (uint32_t)cn, dE + off, dmat + off, thr, S, scomp);
+      if (ce != cudaSuccess) return fail(GF_E_CUDA, "sort count: %s", cudaGetErrorString(ce));
+    }
+    ce = launch_lookup(g, first, (uint32_t)n, seed, dE, dmat, true, S, nullptr, dvsum, scomp, nullptr);
+    if (ce != cudaSuccess) return fail(GF_E_CUDA, "lookup launch: %s", cudaGetErrorString(ce));
+    uint64_t add = 0;
+    GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, scomp));
+    GF_CUDA(cudaStreamSynchronize(scomp));
+    *vsum += add;
+    return GF_OK;
+  }
   const uint64_t nch = (n + kIoChunk - 1) / kIoChunk;
   for (uint64_t c = 0; c < nch; c++) {
     const int k = (int)(c & 1);

@@ -13,6 +13,7 @@
 #include "gf_internal.cuh"
 
 #include <cstdlib>
+#include <cmath>
 
 namespace gf {
 
@@ -189,17 +190,33 @@ static int sort_bits(uint32_t n) {
   return b;
 }
 
+cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) {
+  return cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * (kMats << sort_bits(n)), st);
+}
+
+// Counts caller lookups [0, cn) of a chunk (src_E / src_mat point at the chunk) into the bins of an
+// n_total-lookup batch (no band grids: the host-IO path rejects them).
+cudaError_t launch_sort_count(uint32_t n_total, uint32_t cn, const double *src_E, const uint8_t *src_mat,
+                              const double *thr, const SortScratch &S, cudaStream_t st) {
+  const double inf = HUGE_VAL;
+  const unsigned gc = nblk(((long long)cn + kRunC - 1) / kRunC, 256);
+  sort_count<<<gc, 256, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, sort_bits(n_total));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
                                  cudaStream_t st, double band_lo, double band_hi) {
   cudaError_t e;
   const int nbl = sort_bits(n);
   const int bins = kMats << nbl;  // a multiple of kScanBlk for nbl >= 10
-  if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
-  const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, 256);
   const unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
-  sort_count<<<gc, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!S.counted) {
+    if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
+    const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, 256);
+    sort_count<<<gc, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, nbl);

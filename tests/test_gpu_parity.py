@@ -394,20 +394,25 @@ def test_nuclide_warp_search_edges(gf, torch):
 
 
 def test_host_io_pipeline_chunks(gf, torch):
-    """GF_HOST_IO pipelines chunks of 2^21 lookups over two slots and three streams; with several
-    chunks and a ragged last one the outputs equal the device-resident call's, and the oracle's."""
+    """GF_HOST_IO pipelines chunks of 2^22 lookups over two slots and three streams; with several
+    chunks and a ragged last one the outputs equal the device-resident call's, and the oracle's.
+    Without per-lookup outputs the call runs the whole-batch mode (chunk copies overlap the sort's
+    counting pass; one sort and one lookup pass): its raw sum equals the oracle's over the batch."""
     o, g = make_pair(gf, 68, 11303, O.UNIONIZED)
     rng = np.random.default_rng(21)
-    n = 2 * (1 << 21) + 12345
+    n = 2 * (1 << 22) + 12345
     E = rng.random(n)
     mats = rng.integers(0, 12, n).astype(np.uint8)
     raw_d, m_d = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda())
     raw_h, m_h = g.lookup_energies(torch.from_numpy(E).pin_memory(), torch.from_numpy(mats).pin_memory())
     assert raw_h == raw_d
     assert np.array_equal(m_h.numpy(), m_d.cpu().numpy())
-    sel = np.unique(np.concatenate([rng.integers(0, n, 3000), [0, (1 << 21) - 1, 1 << 21, n - 1]]))
+    sel = np.unique(np.concatenate([rng.integers(0, n, 3000), [0, (1 << 22) - 1, 1 << 22, n - 1]]))
     _, m_o = o.lookup_energies(E[sel], mats[sel].astype(np.int32))
     assert np.array_equal(m_h.numpy()[sel], m_o)
+    raw_w = g.lookup_energies(torch.from_numpy(E).pin_memory(), torch.from_numpy(mats).pin_memory(), want_macro=False)
+    raw_o, _ = o.lookup_energies(E, mats.astype(np.int32))
+    assert raw_w == raw_d == raw_o
 
 
 # ------------------------------------------------------------------------------------------ RSBench

@@ -485,6 +485,11 @@ def test_rs_energies_api(gf, torch):
         assert np.all(np.abs(m_g[t] - m) <= 1e-10 * max(S, 1e-300)), t
         raw_o += O.argmax4_plus1(m)
     assert raw_g == raw_o
+    # host I/O: the chunked pipeline (with per-lookup outputs) and the whole-batch mode (raw only)
+    Eh, mh = torch.from_numpy(E).pin_memory(), torch.from_numpy(mats).pin_memory()
+    raw_h, m_h = g.lookup_energies(Eh, mh)
+    assert raw_h == raw_o and np.array_equal(m_h.numpy(), m_g)
+    assert g.lookup_energies(Eh, mh, want_macro=False) == raw_o
 
 
 @pytest.mark.parametrize("n_iso", [68, 355])

@@ -746,7 +746,8 @@ def main():
         elif not flags:
             kname = f"xs_lookup_direct<{gname}>"
         elif gt == 0:
-            kname = "xs_lookup_warp_nuclide (warp-cooperative search)"
+            kname = ("xs_lookup_sorted<kGridNB> (per-nuclide bin brackets)" if os.environ.get("GF_XS_NB", "1") != "0"
+                     else "xs_lookup_warp_nuclide (warp-cooperative search)")
         else:
             kname = f"xs_lookup_group<{gname}> (+ idx_prep, ~1% of the stage)"
         if HL:

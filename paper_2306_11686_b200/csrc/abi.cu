@@ -173,6 +173,10 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.Rd = take(npts * 8 + 16);  // +16: the staged kernel's bulk copies round ranges up to 16 B
     L.flags = take(16);
     if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128);
+    if (p->grid_type == GF_GRID_NUCLIDE && p->n_gridpoints < 65536) {  // sorted batches search NB brackets
+      L.nb_pitch = ((1 << kNbLog2) + 1 + 63) & ~63;
+      L.NB = take((size_t)p->n_isotopes * L.nb_pitch * 2);
+    }
     if (p->grid_type == GF_GRID_UNIONIZED) {
       // whole grid: all n_iso n_gp energies; band: <= band_cap per nuclide plus the two sentinels
       L.band_cap = band_capacity(p);
@@ -371,8 +375,8 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
       uint32_t *ubin = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint32_t *>(base + L.ubin) : nullptr;
       X.G = G; X.Ed = Ed; X.Rd = Rd; X.XR = XR; X.U = U; X.IG = IG; X.HG = HG; X.ubin = ubin;
-      uint16_t *NB = (X.grid_type == GF_GRID_UNIONIZED && L.nb_pitch) ? reinterpret_cast<uint16_t *>(base + L.NB)
-                                                                       : nullptr;
+      uint16_t *NB = (X.grid_type != GF_GRID_HASH && L.nb_pitch) ? reinterpret_cast<uint16_t *>(base + L.NB)
+                                                                   : nullptr;
       X.NB = NB;
       X.nb_pitch = L.nb_pitch;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;

@@ -143,9 +143,11 @@ __device__ __forceinline__ uint32_t interval(const XsDev &X, uint2 e, double E, 
         if (__ldg(A + mid) <= E) lo = mid + 1; else hi = mid;
       }
       k = lo > 0 ? lo - 1 : 0;
-    } else {
+    } else if (X.IG) {
       const uint32_t nuc = e.y / (uint32_t)X.nb_pitch;
       k = __ldg(X.IG + (size_t)nuc * X.ig_pitch + (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E));
+    } else {  // nuclide grid: the literal search
+      k = bisect<int>(X.Ed + e.x, E, 0, n_gp - 1);
     }
   } else {
     const double *Ed = X.Ed + e.x;
@@ -438,6 +440,12 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
       return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
                        : launch_group<GT, false>(X, n, S, out, vsum, st);
     const char *force = getenv("GF_XS_KERNEL");
+    if (GT == GF_GRID_NUCLIDE && X.NB && use_nb() && !(force && force[0] == 'w')) {  // (w: warp search)
+      if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;
+      xs_lookup_sorted<kGridNB><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
+                                                                               vsum);
+      return cudaGetLastError();
+    }
     if (GT == GF_GRID_NUCLIDE && !(force && force[0] == 't')) {
       if ((e = allow_smem(xs_lookup_warp_nuclide, smem)) != cudaSuccess) return e;
       xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,

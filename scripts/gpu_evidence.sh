@@ -19,5 +19,5 @@ timeout 600 ncu --set full --clock-control none -k regex:xs_lookup_direct -s 3 -
 timeout 600 ncu --set full --clock-control none -k regex:rs_lookup_sorted -s 3 -c 1 -o $O/prof_C5 python bench.py --config C5 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_C5=$?" >> $S
 timeout 600 ncu --set full --clock-control none -k regex:pr_gather -s 3 -c 1 -o $O/prof_P1 python bench.py --config P1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_P1=$?" >> $S
 timeout 600 ncu --set full --clock-control none -k regex:amg_relax -s 3 -c 1 -o $O/prof_A1 python bench.py --config A1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_A1=$?" >> $S
-timeout 600 ncu --set full --clock-control none -k regex:xs_lookup_warp_nuclide -s 3 -c 1 -o $O/prof_C1 python bench.py --config C1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_C1=$?" >> $S
+timeout 600 ncu --set full --clock-control none -k regex:xs_lookup_sorted -s 3 -c 1 -o $O/prof_C1 python bench.py --config C1 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_C1=$?" >> $S
 cat $S

@@ -99,6 +99,8 @@ def test_grid_bytes_closed_form():
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts (sparse batches)
         if gt != gf.NUCLIDE:
             want += al(npts * 128)  # interval records of the sorted kernel
+        else:
+            want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts
         if gt == gf.HASH:
             want += al(n_iso * 10048 * 2)
         want += al(128) + al(64) + al(total * 4) + al(total * 8)

@@ -678,14 +678,15 @@ def test_argmax_robustness_report(gf, torch):
     assert gap_xs > 1e-12 and gap_rs > 1e-8
 
 
-@pytest.mark.parametrize("n_iso", [68, 355])
-def test_nuclide_bin_search_sparse_batches(gf, torch, monkeypatch, n_iso):
+@pytest.mark.parametrize("n_iso,grid_type", [(68, 1), (355, 1), (355, 0)])
+def test_nuclide_bin_search_sparse_batches(gf, torch, monkeypatch, n_iso, grid_type):
     """Sparse batches on a unionized grid (below the group kernel's 4 M threshold) search the
     per-nuclide bin tables NB (#{E_nuc <= b 2^-14}) instead of the index grid.  The table is checked
     against a plain count over the device's energy column, and the lookups -- at NB bin edges, their
     ulp neighbours, exact gridpoints and outside [0, 1), where the kernel falls back to the index
     grid -- against the oracle, with the NB search on and off."""
-    o, g = make_pair(gf, n_iso, 11303, 1)  # (355: the fuel's 321 nuclides take the 3-stage NB ring)
+    o, g = make_pair(gf, n_iso, 11303, grid_type)  # (355: the fuel's 321 nuclides take the 3-stage NB ring;
+    #                                                   nuclide grids use NB for every sorted batch)
     nbt, pitch = g.array("nuclide_bins")
     nb = nbt.cpu().numpy().astype(np.int64).reshape(n_iso, pitch)
     Ed = g.array("energy")[0].cpu().numpy().reshape(n_iso, 11303)

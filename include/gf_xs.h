@@ -217,6 +217,17 @@ gf_status gf_xs_history_batch(const gf_xs_grid *g, uint64_t first_particle, uint
  * interval of the nuclide grid has a normal, non-zero width), 0 when they use __ddiv_rn. */
 gf_status gf_xs_grid_info(const gf_xs_grid *g, int32_t *fastdiv);
 
+/* A/B and test hook: forces the kernel of the sorted lookup path of an XSBench grid (default: chosen
+ * at grid init -- the warp-tile kernel for batches of at least tile_min lookups, one lookup per thread
+ * below).  kern: GF_KERN_AUTO, or one kernel for every batch size; tile_min: the auto crossover
+ * (0 = keep); nb_on: sparse batches and nuclide grids search the per-nuclide bin brackets (1) or the
+ * index grid / warp search (0).  Every choice gives bit-identical results.  Not synchronised with
+ * lookups in flight on the same grid: call it between batches.  GF_E_INVAL for an unknown kernel or
+ * an RSBench grid. */
+enum { GF_KERN_AUTO = 0, GF_KERN_GROUP = 1, GF_KERN_THREAD = 2, GF_KERN_STAGED = 3, GF_KERN_TILE = 4,
+       GF_KERN_TILE_NB = 5, GF_KERN_WARP_SEARCH = 6 };
+gf_status gf_xs_debug_set_kernel(gf_xs_grid *g, int32_t kern, uint64_t tile_min, int32_t nb_on);
+
 /* Diagnostics: d_out[i] = the lookup kernels' reciprocal division of d_a[i] by d_b[i] (device
  * arrays of n doubles), d_ref[i] = IEEE a / b (__ddiv_rn).  The two must agree bit for bit for
  * |a| <= 4 and normal non-zero b.  Enqueued on `stream`. */

@@ -92,6 +92,7 @@ def lib():
             "gf_xs_history_batch": (i32, [vp, u64, u64, i32, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_verify": (i32, [u64, u64, P(u64)]),
             "gf_xs_grid_info": (i32, [vp, P(i32)]),
+            "gf_xs_debug_set_kernel": (i32, [vp, i32, u64, i32]),
             "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
             "gf_xs_last_error": (C.c_char_p, []),
             "gf_pr_graph_bytes": (i32, [C.c_int64, i32, P(sz), P(sz)]),
@@ -196,6 +197,12 @@ class Grid:
         v = C.c_int32()
         _check(lib().gf_xs_grid_info(self.h, C.byref(v)))
         return bool(v.value)
+
+    KERNELS = {"auto": 0, "group": 1, "thread": 2, "staged": 3, "tile": 4, "tilenb": 5, "warp": 6}
+
+    def set_kernel(self, kern: str = "auto", tile_min: int = 0, nb: bool = True):
+        """A/B and test hook (gf_xs_debug_set_kernel): force the sorted-path kernel of this grid."""
+        _check(lib().gf_xs_debug_set_kernel(self.h, self.KERNELS[kern], tile_min, 1 if nb else 0))
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:

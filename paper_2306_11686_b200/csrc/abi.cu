@@ -172,7 +172,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.Ed = take(npts * 8);
     L.Rd = take(npts * 8 + 16);  // +16: the staged kernel's bulk copies round ranges up to 16 B
     L.flags = take(16);
-    if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128);
+    if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128 + 256);  // + the tile kernel's slot overrun
     if (p->grid_type == GF_GRID_NUCLIDE && p->n_gridpoints < 65536) {  // sorted batches search NB brackets
       L.nb_pitch = ((1 << kNbLog2) + 1 + 63) & ~63;
       L.NB = take((size_t)p->n_isotopes * L.nb_pitch * 2);
@@ -220,6 +220,34 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
   L.mconc = take((size_t)(total > 0 ? total : 1) * 8);
   L.total_bytes = o;
   return GF_OK;
+}
+
+// Sorted-path kernel choice, read once per grid here (never on the lookup path).  The environment
+// overrides exist for A/B measurements only; every choice gives identical results.
+//   GF_XS_KERNEL   = tile | tilenb | group | thread | staged | warp   (default: auto)
+//   GF_XS_TILE_MIN = smallest batch of the warp-tile kernel in auto mode (default kTileMinN)
+//   GF_XS_GROUP_MIN = smallest batch of the group kernel in auto mode (default kGroupMinN)
+//   GF_XS_NB       = 0: sparse batches search the index grid instead of the NB brackets
+constexpr uint32_t kTileMinN = 6000000u;   // tools/ab_batch_n.py: tile vs group cross at ~4-8 M lookups
+constexpr uint32_t kGroupMinN = 1500000u;  // group vs one lookup per thread cross at ~1-2 M
+static void kernel_choice(XsDev &X) {
+  static_assert(kKernTile == GF_KERN_TILE && kKernWarpSearch == GF_KERN_WARP_SEARCH, "kernel ids");
+  X.kern = kKernAuto;
+  if (const char *s = getenv("GF_XS_KERNEL")) {
+    const std::string v(s);
+    if (v == "tile") X.kern = kKernTile;
+    else if (v == "tilenb") X.kern = kKernTileNB;
+    else if (v == "group") X.kern = kKernGroup;
+    else if (v == "thread") X.kern = kKernThread;
+    else if (v == "staged") X.kern = kKernStaged;
+    else if (v == "warp") X.kern = kKernWarpSearch;
+  }
+  X.tile_min = kTileMinN;
+  if (const char *m = getenv("GF_XS_TILE_MIN")) X.tile_min = (uint32_t)strtoul(m, nullptr, 10);
+  X.group_min = kGroupMinN;
+  if (const char *m = getenv("GF_XS_GROUP_MIN")) X.group_min = (uint32_t)strtoul(m, nullptr, 10);
+  const char *nb = getenv("GF_XS_NB");
+  X.nb_on = !(nb && nb[0] == '0');
 }
 
 // ------------------------------------------------------------------------------------------ handle
@@ -380,6 +408,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       X.NB = NB;
       X.nb_pitch = L.nb_pitch;
       X.thr = thr; X.moff = moff; X.mnuc = mnuc; X.mconc = mconc;
+      kernel_choice(X);
       const bool banded = X.grid_type == GF_GRID_UNIONIZED && p->n_bands > 1;
       X.k0 = banded ? reinterpret_cast<uint32_t *>(base + L.k0) : nullptr;
       const double inf = 1.0 / 0.0;
@@ -480,7 +509,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, h_macro, h_E, h_mat, bytes;
+  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, work, h_macro, h_E, h_mat, bytes;
 };
 struct BatchLayout {
   SlotLayout slot;
@@ -529,6 +558,7 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
     L.idx = take(sizeof(uint32_t) * m);
     L.us = take(sizeof(uint32_t) * m);
     L.tinfo = take(32 * ((m + 127) / 128));
+    L.work = take(256);
   }
   if (host_io) {
     if (want_macro) L.h_macro = take(sizeof(double) * ch * m);
@@ -558,6 +588,7 @@ static SortScratch slot_sort(char *base, const SlotLayout &L) {
   S.idx = reinterpret_cast<uint32_t *>(base + L.idx);
   S.us = reinterpret_cast<uint32_t *>(base + L.us);
   S.tinfo = base + L.tinfo;
+  S.work = reinterpret_cast<uint32_t *>(base + L.work);
   return S;
 }
 
@@ -832,6 +863,17 @@ gf_status gf_xs_selftest_div(const double *d_a, const double *d_b, double *d_out
   if (n == 0) return GF_OK;
   cudaError_t ce = launch_div_selftest(d_a, d_b, d_out, d_ref, (int)n, reinterpret_cast<cudaStream_t>(stream));
   if (ce != cudaSuccess) return fail(GF_E_CUDA, "selftest launch: %s", cudaGetErrorString(ce));
+  return GF_OK;
+}
+
+gf_status gf_xs_debug_set_kernel(gf_xs_grid *g, int32_t kern, uint64_t tile_min, int32_t nb_on) {
+  if (!g) return fail(GF_E_INVAL, "grid is NULL");
+  if (g->p.bench != GF_XSBENCH) return fail(GF_E_INVAL, "kernel choice applies to XSBench grids");
+  if (kern < GF_KERN_AUTO || kern > GF_KERN_WARP_SEARCH) return fail(GF_E_INVAL, "unknown kernel %d", kern);
+  if (tile_min >= (1ull << 32)) return fail(GF_E_INVAL, "tile_min %llu >= 2^32", (unsigned long long)tile_min);
+  g->xs.kern = kern;
+  if (tile_min) g->xs.tile_min = (uint32_t)tile_min;
+  g->xs.nb_on = nb_on ? 1 : 0;
   return GF_OK;
 }
 

@@ -394,31 +394,20 @@ __global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(X
 #include "xs_sorted_u.cuh"
 #include "xs_warp_nuclide.cuh"
 
-// Kernel for the sorted path.  Default: the persistent group kernel (kL lookups per thread sharing
-// record loads) for dense batches, n >= kGroupMinN, and the one-lookup-per-thread kernel below it:
-// a sparse batch (a history wave, a host-IO chunk) has few lookups per interval, so record sharing
-// buys little while the group kernel's 4x fewer threads leave the DRAM latency exposed (measured,
-// DESIGN.md Sec. 7).  The nuclide grid uses the warp-cooperative search kernel.  GF_XS_KERNEL in the
-// environment forces an alternative for A/B measurements ("group", "thread", "staged" = the TMA
-// producer/consumer ring, unionized only); GF_XS_GROUP_MIN overrides the threshold.  All give
-// identical results.  (Read on every launch: the tests and A/B tools switch it within a process.)
-enum { kKernGroup = 0, kKernStaged = 1, kKernThread = 2 };
-constexpr uint32_t kGroupMinN = 4u << 20;  // crossover measured at ~4 M (tools/ab_batch_n.py)
-static int sorted_kernel(uint32_t n) {
-  const char *s = getenv("GF_XS_KERNEL");
-  if (s && s[0] == 's') return kKernStaged;
-  if (s && s[0] == 't') return kKernThread;
-  if (s && s[0] == 'g') return kKernGroup;
-  const char *m = getenv("GF_XS_GROUP_MIN");
-  const uint32_t nmin = m ? (uint32_t)strtoul(m, nullptr, 10) : kGroupMinN;
-  return n >= nmin ? kKernGroup : kKernThread;
-}
+#include "xs_tile.cuh"
 
-// Sparse batches on a unionized grid (below kGroupMinN: history waves, host-IO chunks) search the
-// per-nuclide bin tables instead of the index grid; GF_XS_NB=0 in the environment disables it (A/B).
-static bool use_nb() {
-  const char *s = getenv("GF_XS_NB");
-  return !(s && s[0] == '0');
+// Kernel for the sorted path (XsDev::kern, chosen once at grid init).  Default: the warp-tile kernel
+// for dense batches (n >= tile_min; unionized and hash grids), the group kernel (4 lookups per
+// thread, per-lookup searches) for medium ones and the one-lookup-per-thread kernel below group_min:
+// a sparse batch (a history wave, a host-IO chunk) spreads a tile over many intervals, beyond its
+// staged records (measured).  The nuclide grid searches the
+// per-nuclide bin brackets (NB).  The alternatives stay selectable for A/B measurements
+// (GF_XS_KERNEL at grid init): group (4 lookups per thread, per-lookup index-grid loads), thread,
+// staged (TMA producer / consumer ring, unionized), tilenb (tile runs from the NB brackets), warp
+// (warp-cooperative nuclide-grid search).
+static int sorted_kernel(const XsDev &X, uint32_t n) {
+  if (X.kern != kKernAuto) return X.kern;
+  return n >= X.tile_min ? kKernTile : n >= X.group_min ? kKernGroup : kKernThread;
 }
 
 template <int GT>
@@ -432,27 +421,35 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
         cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    const int kern = sorted_kernel(n);
+    const int kern = sorted_kernel(X, n);
     if (GT == GF_GRID_UNIONIZED && kern == kKernStaged)
       return X.fastdiv ? launch_staged<true>(X, n, S, out, vsum, st)
                        : launch_staged<false>(X, n, S, out, vsum, st);
     if (GT != GF_GRID_NUCLIDE && kern == kKernGroup)
       return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
                        : launch_group<GT, false>(X, n, S, out, vsum, st);
-    const char *force = getenv("GF_XS_KERNEL");
-    if (GT == GF_GRID_NUCLIDE && X.NB && use_nb() && !(force && force[0] == 'w')) {  // (w: warp search)
+    if constexpr (GT != GF_GRID_NUCLIDE) {
+      if (kern == kKernTile)
+        return X.fastdiv ? launch_tile<GT, true>(X, n, S, out, vsum, st) : launch_tile<GT, false>(X, n, S, out, vsum, st);
+    }
+    if constexpr (GT == GF_GRID_UNIONIZED) {
+      if (kern == kKernTileNB && X.NB)
+        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st)
+                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st);
+    }
+    if (GT == GF_GRID_NUCLIDE && X.NB && X.nb_on && kern != kKernWarpSearch) {
       if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;
       xs_lookup_sorted<kGridNB><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                                vsum);
       return cudaGetLastError();
     }
-    if (GT == GF_GRID_NUCLIDE && !(force && force[0] == 't')) {
+    if (GT == GF_GRID_NUCLIDE && kern != kKernThread) {
       if ((e = allow_smem(xs_lookup_warp_nuclide, smem)) != cudaSuccess) return e;
       xs_lookup_warp_nuclide<<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                            vsum);
       return cudaGetLastError();
     }
-    if (GT == GF_GRID_UNIONIZED && X.NB && use_nb()) {
+    if (GT == GF_GRID_UNIONIZED && X.NB && X.nb_on) {
       if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;
       xs_lookup_sorted<kGridNB><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,
                                                                                vsum);

@@ -267,11 +267,21 @@ __device__ __forceinline__ void group_loop(const XsDev &X, const XsTables &T, co
   }
 }
 
+// Dynamic work distribution (group and tile kernels): lane 0 of a warp takes the next unit of 32
+// groups (128 lookups) from a per-launch counter.  Work units come in sorted order, i.e. the
+// 321-nuclide fuel first, so the heavy units are handed out first and warps finish together
+// (a static grid-stride split left SMs idle for ~25% of the kernel, ncu active vs elapsed cycles).
+__device__ __forceinline__ uint32_t next_tile(uint32_t *work) {
+  uint32_t t = 0;
+  if ((threadIdx.x & 31) == 0) t = atomicAdd(work, 1u);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
+
 template <int GT, bool FAST>
 __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
     xs_lookup_group(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
                     const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart,
-                    OutSpec out, unsigned long long *__restrict__ vsum) {
+                    OutSpec out, unsigned long long *__restrict__ vsum, uint32_t *__restrict__ work) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t ms[kMats + 1];  // material segment starts (SMEM: registers go to the loop)
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
@@ -279,7 +289,9 @@ __global__ void __launch_bounds__(kTpbL, GF_GROUP_MINB)
   n = min(n, ms[kMats]);  // lookups kept by the sort (band grids keep their band's)
   uint32_t vacc = 0;
   const uint32_t ngroups = (n + kL - 1) / kL;
-  for (uint32_t g = blockIdx.x * kTpbL + threadIdx.x; g < ngroups; g += gridDim.x * kTpbL) {
+  for (uint32_t wg = next_tile(work); wg * 32 < ngroups; wg = next_tile(work)) {
+    const uint32_t g = wg * 32 + (threadIdx.x & 31);
+    if (g >= ngroups) continue;
     const uint32_t p0 = g * kL;
     const uint32_t nl = min((uint32_t)kL, n - p0);
     int mat0 = 0, mat1 = 0;
@@ -361,6 +373,7 @@ static cudaError_t launch_group(const XsDev &X, uint32_t n, const SortScratch &S
   const uint32_t grid = min((ngroups + kTpbL - 1) / kTpbL, (uint32_t)(sms * max(blocks_per_sm, 1)));
   idx_prep<GT><<<nblk(((long long)n + 3) / 4, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum);
+  if ((e = cudaMemsetAsync(S.work, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
+  xs_lookup_group<GT, FAST><<<grid, kTpbL, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum, S.work);
   return cudaGetLastError();
 }

@@ -217,23 +217,21 @@ def test_C2_small_unionized(gf):
     assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
 
 
-@pytest.mark.parametrize("kernel,grid", [("staged", 1), ("thread", 1), ("thread", 0)])
+@pytest.mark.parametrize("kernel,grid", [("staged", 1), ("thread", 1), ("group", 1), ("tile", 1), ("tilenb", 1),
+                                         ("thread", 0), ("warp", 0), ("group", 2), ("tile", 2)])
 def test_alternative_sorted_kernels_match(gf, kernel, grid):
-    """GF_XS_KERNEL selects the alternative kernels of the sorted unionized path (the TMA-staged
-    producer/consumer ring, the non-persistent per-thread kernel); they must give the oracle's bits
-    too (run in a child process: the switch is read once)."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, oracle as O, paper_2306_11686_b200 as gf\n"
-        f"o = O.XSOracle(355, 11303, {grid}); g = gf.Grid(gf.Params.xsbench(355, 11303, {grid}))\n"
-        "r1, m1 = o.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
-        "r2, m2 = g.lookup_batch(3_000_000, 200_000, want_macro=True)\n"
-        "assert r1 == r2 and np.array_equal(m1, m2.cpu().numpy())\n"
-        "print('ok')\n")
-    env = dict(os.environ, GF_XS_KERNEL=kernel, PYTHONPATH=os.path.dirname(HERE))
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
+    """gf_xs_debug_set_kernel forces one kernel of the sorted path for every batch size (the TMA-staged
+    producer/consumer ring, the per-thread kernel, the 4-lookups-per-thread group kernel, the warp-tile
+    kernel with index-grid or NB runs, the warp-cooperative nuclide search); each must give the
+    oracle's bits.  At 200 k lookups a tile spans many intervals per nuclide, so the tile kernel's
+    runs overflow kNbMax and its per-lookup search fallback runs too."""
+    o = O.XSOracle(355, 11303, grid)
+    g = gf.Grid(gf.Params.xsbench(355, 11303, grid))
+    g.set_kernel(kernel)
+    for first, n in ((3_000_000, 200_000), (0, 2_125_000)):
+        r1, m1 = o.lookup_batch(first, n, want_macro=True)
+        r2, m2 = g.lookup_batch(first, n, want_macro=True)
+        assert r1 == r2 and np.array_equal(m1, m2.cpu().numpy()), (first, n)
 
 
 def test_small_hash_grid(gf):
@@ -355,12 +353,14 @@ def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
             Es += [e + d * 2.0 ** -40 for d in (-3, -1, 0, 1, 3)]
     Es += list(0.3 + rng.random(20000) * 1e-3)  # dense: about 20 lookups per interval per nuclide
     E = np.clip(np.array(Es), 0.0, 1.0)
-    for mat in (0, 4, 7):
-        mats = np.full(len(E), mat, dtype=np.uint8)
-        raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
-        raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
-        assert raw_g == raw_o
-        assert np.array_equal(m_g.cpu().numpy(), m_o), f"mat {mat}"
+    for kern in ("auto", "tile", "group"):  # the warp-tile kernel's runs (R-TILE) see the same clusters
+        g.set_kernel(kern)
+        for mat in (0, 4, 7):
+            mats = np.full(len(E), mat, dtype=np.uint8)
+            raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
+            raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
+            assert raw_g == raw_o, (kern, mat)
+            assert np.array_equal(m_g.cpu().numpy(), m_o), f"{kern} mat {mat}"
 
 
 def test_nuclide_warp_search_edges(gf, torch):
@@ -381,7 +381,8 @@ def test_nuclide_warp_search_edges(gf, torch):
     Es += list(rng.random(40))                             # wide warps
     Es += [0.0, 1.0, -0.5, 3.0, math.inf, -math.inf, 5e-324, -0.0]
     E = np.array(Es)
-    for mat in (0, 4, 7):
+    for kern, mat in [("warp", 0), ("warp", 4), ("warp", 7), ("auto", 0), ("auto", 7)]:  # auto: NB brackets
+        g.set_kernel(kern)
         for extra in ([], [math.nan, math.nan, 0.5]):
             EE = np.concatenate([E, np.array(extra, dtype=np.float64)])
             mats = np.full(len(EE), mat, dtype=np.uint8)
@@ -679,7 +680,7 @@ def test_argmax_robustness_report(gf, torch):
 
 
 @pytest.mark.parametrize("n_iso,grid_type", [(68, 1), (355, 1), (355, 0)])
-def test_nuclide_bin_search_sparse_batches(gf, torch, monkeypatch, n_iso, grid_type):
+def test_nuclide_bin_search_sparse_batches(gf, torch, n_iso, grid_type):
     """Sparse batches on a unionized grid (below the group kernel's 4 M threshold) search the
     per-nuclide bin tables NB (#{E_nuc <= b 2^-14}) instead of the index grid.  The table is checked
     against a plain count over the device's energy column, and the lookups -- at NB bin edges, their
@@ -708,6 +709,6 @@ def test_nuclide_bin_search_sparse_batches(gf, torch, monkeypatch, n_iso, grid_t
     mats = np.concatenate([mats, rng.integers(0, 12, len(extra)).astype(np.uint8)])
     raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
     for flag in ("1", "0"):
-        monkeypatch.setenv("GF_XS_NB", flag)
+        g.set_kernel("auto", nb=flag == "1")
         raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
         assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o), flag

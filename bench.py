@@ -9,10 +9,13 @@ the rank's shard of the config's event lookups: sample -> locality sort -> searc
 accumulate -> hash reduction, then the cross-rank int64 all-reduce of the raw hash (NCCL) when
 N > 1.  The grid build (A0) runs once before timing and is reported separately (grid_build_ms),
 like the paper's kernel-only timing.  Default workload: C3 = XSBench large,
-unionized grid, 17 M lookups (BASELINE.json configs[2], the north_star's target), weak-scaled
-over N ranks by default (every rank runs 17 M lookups from its own global index range; --scaling
-strong splits the 17 M instead).  Every step is timed with CUDA events on the launching stream; L2 is flushed by a
-256 MiB write between steps (outside the events).  Rank 0 prints one JSON line.
+unionized grid, 17 M lookups (BASELINE.json configs[2], the north_star's target), strong-scaled
+over N ranks by default (rank r runs the global indices [floor(r n / N), floor((r+1) n / N)) of the
+config's n lookups; --scaling weak gives every rank its own n-lookup range
+instead).  At N = 1 the line also carries strong_proxy: the per-rank step of the 2 / 4 / 8-way
+split timed on this one GPU (every shard, the slowest counts).  Every step is timed with CUDA events
+on the launching stream; L2 is flushed by a 256 MiB write between steps (outside the events).  Rank
+0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -54,6 +57,19 @@ CONFIGS = {
     "H5": ("rs", 355, None, 10_200_000, "RSBench large 355 nuclides, HISTORY mode 300k particles x 34 lookups"),
 }
 HIST_L = {"H2": 34, "H3": 34, "H5": 34}  # lookups per particle (history configs)
+# The paper's own numbers for the same benchmark and mode (context only): kernel speedup
+# of GPU First / manual offload over the CPU OpenMP parallel region, A100-40GB vs AMD EPYC 7532.
+PAPER = {
+    "xs_event_small": {"gpu_first": 11.772, "manual_offload": 9.757, "cite": "PAPER.md:1185,1193 (Fig. 8a)"},
+    "xs_event_large": {"gpu_first": 11.434, "manual_offload": 11.503, "cite": "PAPER.md:1223,1231 (Fig. 8a)"},
+    "xs_history_small": {"gpu_first": 14.360, "cite": "PAPER.md:1210 (Fig. 8a)"},
+    "xs_history_large": {"gpu_first": 10.64, "cite": "PAPER.md:1247 (Fig. 8a)"},
+    "rs_event_large": {"gpu_first": 4.6102, "manual_offload": 4.5159, "cite": "PAPER.md:1342,1350 (Fig. 8b)"},
+    "rs_history_large": {"gpu_first": 4.6277, "cite": "PAPER.md:1366 (Fig. 8b)"},
+}
+PAPER_KEY = {"C1": "xs_event_small", "C2": "xs_event_small", "C3": "xs_event_large", "C4": "xs_event_large",
+             "C3N": "xs_event_large", "C5": "rs_event_large", "C5D0": "rs_event_large", "H2": "xs_history_small",
+             "H3": "xs_history_large", "H5": "rs_history_large"}
 # Per-lookup algorithmic work of the dominant kernel:
 #   sector bytes of the random-order gather model, and fp64 flops (division counted as 1).
 #   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
@@ -71,12 +87,12 @@ def oracle_run(o, cfg, first, n, threads):
     return o.lookup_batch(first, n, threads=threads), n
 
 
-def launches_per_step(bench, gt, sorted_):
+def launches_per_step(bench, gt, sorted_, kern=""):
     """Our kernels per step: sort_count, scan_local, scan_add, sort_scatter (A1-A2), then the lookup
-    kernel; the unionized / hash group kernel is preceded by idx_prep (A3)."""
+    kernel; the unionized / hash tile and group kernels are preceded by idx_prep (A3)."""
     if not sorted_:
         return 1
-    return 4 + (2 if (bench == "xs" and gt in (1, 2)) else 1)
+    return 4 + (2 if (bench == "xs" and gt in (1, 2) and kern in ("tile", "group", "")) else 1)
 
 
 def load_profile(cfg, sorted_):
@@ -281,6 +297,7 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
     """C7: every rank builds, in turn, the band replicas of its bands (r, r + N, ... of W = 8; grid build
     untimed), and runs the full event batch through each -- the sort keeps the band's lookups.  A step
     is one batch through all of the rank's bands; value = 17 M / max-over-ranks step time."""
+    from paper_2306_11686_b200 import dist as gdist
     W, n = 8, CONFIGS["C7"][3]
     mine = list(range(rank, W, world))
     st = torch.cuda.current_stream()
@@ -310,10 +327,8 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
     step_ms = sum(per_band)
     rv = torch.tensor([raws], dtype=torch.int64, device=dev)
     if dist is not None:
-        dist.all_reduce(rv)
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = t.item()
+        gdist.reduce_raw(rv)
+        step_ms = gdist.max_over_ranks([step_ms], dev)[0]
     if rank == 0:
         peaks = load_peaks()
         look_s = step_ms * 1e-3
@@ -339,6 +354,7 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
 def bench_pagerank(args, rank, world, dev, gf, torch, dist):
     """P1 (NEXT-4): one step = contributions + in-edge gather over the whole graph (include/gf_pr.h).
     Every rank runs its own replica (weak scaling; independent problems, no exchange)."""
+    from paper_2306_11686_b200 import dist as gdist
     import numpy as np
     n, D = CONFIGS["P1"][1], CONFIGS["P1"][2]
     t0 = time.perf_counter()
@@ -365,9 +381,7 @@ def bench_pagerank(args, rank, world, dev, gf, torch, dist):
     ts = [e0.elapsed_time(e1) for e0, e1 in evs[args.warmup:]]
     step_ms = sum(ts) / len(ts)
     if dist is not None:
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = t.item()
+        step_ms = gdist.max_over_ranks([step_ms], dev)[0]
     # end to end through the public API: ranks in from pinned host memory, result back
     e2e = None
     if not args.no_e2e:
@@ -425,6 +439,7 @@ def bench_pagerank(args, rank, world, dev, gf, torch, dist):
 
 def bench_amg(args, rank, world, dev, gf, torch, dist):
     """A1 (NEXT-4): one relaxation sweep over the whole matrix (include/gf_amg.h); replicas per rank."""
+    from paper_2306_11686_b200 import dist as gdist
     import numpy as np
     nx, ny, nz = CONFIGS["A1"][1:4]
     A = gf.AMGMatrix(nx, ny, nz, device=dev.index)
@@ -449,9 +464,7 @@ def bench_amg(args, rank, world, dev, gf, torch, dist):
         torch.cuda.synchronize()
     step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs[args.warmup:]) / args.steps
     if dist is not None:
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = t.item()
+        step_ms = gdist.max_over_ranks([step_ms], dev)[0]
     e2e = None
     if not args.no_e2e:
         uh = torch.from_numpy(rng.random(n)).pin_memory()
@@ -511,9 +524,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank runs the config's lookups (global indices [r n, (r+1) n)); "
-                         "strong: the config's lookups are split over the ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the config's lookups are split over the ranks (SURVEY.md 8(e)); "
+                         "weak: every rank runs the config's lookups (global indices [r n, (r+1) n))")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the N=1 strong-scaling proxies (W = 2, 4, 8)")
     ap.add_argument("--no-sort", action="store_true", help="skip the A2 locality sort (unsorted gather kernel)")
     ap.add_argument("--hist-mode", default="sorted", choices=["sorted", "waves", "direct"],
                     help="history configs: sorted step waves (default), unsorted waves, or one thread per particle")
@@ -534,6 +548,7 @@ def main():
     import torch
     import paper_2306_11686_b200 as gf
     from paper_2306_11686_b200 import build as gfbuild
+    from paper_2306_11686_b200 import dist as gdist
     if rank == 0 and gfbuild.needs_build():
         gfbuild.build()
     # one process per GPU; GF_DIST_BACKEND=gloo lets several ranks share one GPU (path tests only)
@@ -561,7 +576,16 @@ def main():
             dist.destroy_process_group()
         return
     bench, n_iso, gt, n_total, desc = CONFIGS[args.config]
-    if args.scaling == "weak":
+    HL = HIST_L.get(args.config)
+    if HL:  # history mode: the unit of work is a particle (HL dependent lookups); shard whole particles
+        p_total = n_total // HL
+        if args.scaling == "weak":
+            np_first, n_part = gf.weak_range(p_total, rank)
+            p_total *= world
+        else:
+            np_first, n_part = gf.shard_range(p_total, rank, world)
+        n_total, first, n = p_total * HL, np_first * HL, n_part * HL
+    elif args.scaling == "weak":
         first, n = gf.weak_range(n_total, rank)
         n_total = n * world
     else:
@@ -580,10 +604,8 @@ def main():
     grid_ms = e0.elapsed_time(e1)
 
     flags = 0 if args.no_sort else gf.SORT_LOCALITY
-    HL = HIST_L.get(args.config)
-    if HL:  # history mode: the unit of work is a particle (HL dependent lookups)
+    if HL:
         flags = gf.Grid.HIST_MODES[args.hist_mode]
-        np_first, n_part = first // HL, n // HL
         hb = C.c_size_t()
         gf._check(gf.lib().gf_xs_history_bytes(grid.h, n_part, flags, C.byref(hb)))
         scratch = torch.empty(max(hb.value, 256), dtype=torch.uint8, device=dev)
@@ -627,7 +649,7 @@ def main():
                                                 scratch.numel(), C.c_void_p(st.cuda_stream)))
             ev[2].record()
             if dist is not None:
-                dist.all_reduce(vsum)
+                gdist.reduce_raw(vsum)
             ev[3].record()
             return
         se = (C.c_void_p * 3)(ev[0].cuda_event, ev[1].cuda_event, ev[2].cuda_event)
@@ -635,7 +657,7 @@ def main():
                                           C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
                                           scratch.numel(), C.c_void_p(st.cuda_stream), se))
         if dist is not None:
-            dist.all_reduce(vsum)
+            gdist.reduce_raw(vsum)
         ev[3].record()
 
     # events must be created before use: touch them
@@ -667,12 +689,46 @@ def main():
     look_ms = [evs[k][1].elapsed_time(evs[k][2]) for k in range(args.warmup, args.warmup + K)]
     tot_ms = sum(step_ms)
     if dist is not None:
-        t = torch.tensor([tot_ms, sum(look_ms)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, look_tot = t.tolist()
+        tot_ms, look_tot = gdist.max_over_ranks([tot_ms, sum(look_ms)], dev)
     else:
         look_tot = sum(look_ms)
     value = n_total * K / (tot_ms * 1e-3)
+
+    # ---------------------------------------------------------------- strong-scaling proxies (N = 1)
+    # The per-rank step of the W-way split of this config (rank r takes
+    # [floor(r n / W), floor((r+1) n / W))), every shard timed on this one GPU exactly as a rank runs it
+    # (same call, same flags; L2 flushed before each rep).  The slowest shard bounds a W-GPU step, so
+    # speedup = T_1 / max shard; the W-GPU step adds one 8-B all-reduce (~10-30 us over NVLink).
+    proxy = None
+    if (world == 1 and not args.no_proxy and not HL and args.scaling == "strong" and bench in ("xs", "rs")
+            and n_total >= 1_000_000):
+        T1 = tot_ms / K
+        proxy = {"T1_ms": T1}
+        for W in (2, 4, 8):
+            shard_ms, raw_w = [], 0
+            for r in range(W):
+                lo, cnt = gf.shard_range(n_total, r, W)
+                ts = []
+                for k in range(4):  # 1 warm-up + 3 timed
+                    flush.fill_(k & 0xFF)
+                    vsum.zero_()
+                    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    p0.record()
+                    gf._check(L.gf_xs_lookup_batch(grid.h, lo, cnt, gf.STARTING_SEED, flags, None,
+                                                   C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                                   scratch.numel(), C.c_void_p(st.cuda_stream)))
+                    p1.record()
+                    torch.cuda.synchronize()
+                    if k:
+                        ts.append(p0.elapsed_time(p1))
+                raw_w += int(vsum.item())
+                shard_ms.append(statistics.median(ts))
+            mx = max(shard_ms)
+            proxy[str(W)] = {"lookups_per_rank": n_total // W, "max_shard_ms": mx, "speedup": T1 / mx,
+                             "kernel": grid.kernel_for(n_total // W, flags) if bench == "xs" else "rs_lookup_sorted",
+                             "shard_ms": [round(x, 4) for x in shard_ms], "hash": gf.verify(raw_w)}
+        proxy["note"] = ("per-rank step (sort + lookup) of the W-way strong split, each shard timed on this GPU; "
+                         "speedup = T1 / slowest shard (excludes the 8-B all-reduce)")
 
     # ---------------------------------------------------------------- end-to-end through the public API
     e2e = None
@@ -686,12 +742,10 @@ def main():
             r_e2e = grid.history_batch(np_first, n_part, HL, mode=args.hist_mode)
             if dist is not None:
                 rt = torch.tensor([r_e2e], dtype=torch.int64, device=dev)
-                dist.all_reduce(rt)
+                gdist.reduce_raw(rt)
         el = time.perf_counter() - t0
         if dist is not None:
-            t = torch.tensor([el], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = t.item()
+            el = gdist.max_over_ranks([el], dev)[0]
         e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
                "path": "Grid.history_batch (gf_xs_history_batch): particle indices + seed in, raw sum (8 B) out; "
                        "host-timed incl. launch and sync"}
@@ -716,12 +770,10 @@ def main():
                 r_e2e = r_e2e[0] if want_macro else r_e2e
                 if dist is not None:
                     rt = torch.tensor([r_e2e], dtype=torch.int64, device=dev)
-                    dist.all_reduce(rt)
+                    gdist.reduce_raw(rt)
             el = time.perf_counter() - t0
             if dist is not None:
-                t = torch.tensor([el], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                el = t.item()
+                el = gdist.max_over_ranks([el], dev)[0]
             return n_total * reps / el
 
         # the step's result is the verification value (XSBench's output); the macro variant also returns
@@ -741,15 +793,18 @@ def main():
         per_launch_lookups = n  # one lookup-kernel launch per step per rank
         look_avg_s = look_tot / K * 1e-3
         gname = {0: "nuclide", 1: "unionized", 2: "hash"}.get(gt, "")
+        kern = grid.kernel_for(n, flags) if (bench == "xs" and not HL) else ""
         if bench == "rs":
             kname = "rs_lookup_sorted" if flags else "rs_lookup_direct"
         elif not flags:
             kname = f"xs_lookup_direct<{gname}>"
         elif gt == 0:
-            kname = ("xs_lookup_sorted<kGridNB> (per-nuclide bin brackets)" if os.environ.get("GF_XS_NB", "1") != "0"
+            kname = ("xs_lookup_sorted<kGridNB> (per-nuclide bin brackets)" if kern == "thread"
                      else "xs_lookup_warp_nuclide (warp-cooperative search)")
         else:
-            kname = f"xs_lookup_group<{gname}> (+ idx_prep, ~1% of the stage)"
+            kname = {"tile": f"xs_lookup_tile<{gname}> (warp tiles, SMEM-staged interval runs; + idx_prep)",
+                     "group": f"xs_lookup_group<{gname}> (+ idx_prep)",
+                     "thread": "xs_lookup_sorted<kGridNB> (one lookup per thread)"}.get(kern, kern)
         if HL:
             kname = ({"direct": f"{bench}_history_direct (one thread per particle, {HL} dependent lookups)"}.get(
                 args.hist_mode, f"{HL} waves of hist_sample + " + ("sort + " if flags & gf.SORT_LOCALITY else "")
@@ -760,28 +815,34 @@ def main():
                 "achieved": flops / look_avg_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
                 "unit": "TFLOP/s", "traffic": prof.get("dram_bytes") if prof else None,
                 "note": f"{alg_flops} fp64 flops/lookup (DESIGN.md Sec. 5; division counted once) x "
-                        f"{per_launch_lookups} lookups per launch / mean stage time (CUDA events on the launch "
-                        f"stream); peak = measured non-FMA FP64 op rate ({peaks['probe_src']}); traffic = ncu "
-                        f"dram read+write bytes per launch ({prof.get('src') if prof else 'no capture'})"}
+                        f"{per_launch_lookups} lookups per launch / mean lookup-stage time (CUDA events on the "
+                        f"launch stream); peak = measured non-FMA FP64 op rate ({peaks['probe_src']}); traffic = "
+                        f"ncu dram read+write bytes per launch ({prof.get('src') if prof else 'no capture'})"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof_hbm = None
-        if alg_bytes:
-            gb = alg_bytes * per_launch_lookups / look_avg_s / 1e9
-            roof_hbm = {"bound": "hbm", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": gb / peaks["hbm_gbs"], "note": f"{alg_bytes} B/lookup random-order sector model "
-                        f"(SURVEY 8(d)); >1 means the sort removed algorithmic bytes ({peaks['src']})"}
-            if prof and prof.get("dram_bytes"):
-                roof_hbm["dram_GBps_measured"] = prof["dram_bytes"] / look_avg_s / 1e9
-        roof_gather = None
-        if alg_bytes and peaks.get("gather96_GBps"):
-            # the north_star's "fraction of the HBM random-gather roofline" (SURVEY.md 8(d) R-ROOF rho_thru):
-            # whole-step lookups/s x the random-order sector bytes per lookup / the measured random 96-B
-            # record-pair gather bandwidth (tools/roofline_probe.cu, K6); > 1 because the sort removes the gather
-            gb = value / world * alg_bytes / 1e9
-            roof_gather = {"bound": "gather", "achieved": gb, "peak": peaks["gather96_GBps"], "unit": "GB/s",
-                           "frac": gb / peaks["gather96_GBps"],
-                           "note": f"R-ROOF rho_thru: per-GPU lookups/s x {alg_bytes} B / measured random 96-B "
-                                   f"record-pair gather bandwidth ({peaks['probe_src']})"}
+        # SURVEY.md 8(d) R-ROOF: the four numbers per run.  rho_thru divides the random-order sector bytes
+        # per lookup by the measured random-gather bandwidth (K6, tools/roofline_probe.cu) -- it can exceed
+        # 1 because the locality sort removes those bytes, so it is never a DRAM fraction; rho_dram /
+        # rho_L2 / l2_hit come from the committed ncu capture of the dominant kernel (src, kernel).
+        rho = None
+        if bench == "xs" or prof:
+            rho = {"rho_fp64_live": roof["frac"]}
+            if alg_bytes and peaks.get("gather96_GBps"):
+                gb = value / world * alg_bytes / 1e9
+                rho.update(rho_thru=gb / peaks["gather96_GBps"], gather_GBps=peaks["gather96_GBps"],
+                           alg_sector_bytes_per_lookup=alg_bytes)
+            if prof:
+                dur = prof.get("duration_s") or 0
+                rho.update(rho_dram=(prof["dram_bytes"] / dur / 1e9 / peaks["hbm_gbs"]) if dur else None,
+                           dram_GBps=(prof["dram_bytes"] / dur / 1e9) if dur else None,
+                           rho_L2=(prof["lts_pct"] / 100) if prof.get("lts_pct") is not None else None,
+                           l2_hit_pct=prof.get("l2_hit_pct"),
+                           rho_fp64_ncu=(prof["fp64_pipe_pct"] / 100) if prof.get("fp64_pipe_pct") else None,
+                           capture=prof.get("src"), capture_kernel=prof.get("kernel", "")[:60])
+        paper = None
+        if args.config in PAPER_KEY:
+            paper = dict(PAPER[PAPER_KEY[args.config]], hardware="NVIDIA A100 40GB vs AMD EPYC 7532 (PAPER.md:812)",
+                         metric="kernel speedup over the CPU OpenMP parallel region (PAPER.md:1069)",
+                         note="context only: other hardware, and the paper's CPU baseline is the original program")
         cb = None
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_baseline(args.config)
@@ -799,9 +860,9 @@ def main():
                        "parallelism": f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, {first + n}) on rank 0), "
                                       f"grid replicated, 1 int64 "
                                       f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
-            "roofline": roof, "roofline_hbm_model": roof_hbm, "roofline_gather": roof_gather,
+            "roofline": roof, "rho": rho, "strong_proxy": proxy, "paper_context": paper,
             "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY) if not HL else
+            "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY, kern) if not HL else
                                  (1 if args.hist_mode == "direct" else
                                   HL * (1 + launches_per_step(bench, gt, flags & gf.SORT_LOCALITY)))),
             "clocks": clk,

@@ -152,8 +152,15 @@ enum {
                                    particle runs its L lookups back to back */
 };
 
-/* Scratch bytes a lookup call of n lookups with `flags` needs (caller allocates on the device). */
+/* Scratch bytes a lookup call of n lookups with `flags` needs (caller allocates on the device).  With
+ * GF_HOST_IO this is the chunked pipeline's bound (two 2^22-lookup chunk slots): device memory does not
+ * grow with n. */
 gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes);
+/* The larger scratch of the whole-batch host-I/O mode (gf_xs_lookup_energies, GF_HOST_IO |
+ * GF_SORT_LOCALITY, no per-lookup outputs): the chunk copies overlap the sort's counting pass, then one
+ * sort and one lookup pass run over the whole batch (O(n) device scratch, ~25 B per lookup).  A call
+ * given at least this much scratch runs that mode; with less, the chunked pipeline (same results). */
+gf_status gf_xs_batch_bytes_whole(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes);
 
 /* A1-A6 / B1-B4: event-based lookups with GLOBAL indices [first, first+n).
  * Lookup i samples (E, material) from the LCG stream fast_forward(starting_seed, 2i) (1070 in the
@@ -183,8 +190,14 @@ gf_status gf_xs_lookup_batch_ev(const gf_xs_grid *g, uint64_t first, uint64_t n,
                                 size_t scratch_bytes, gf_stream_t stream, const gf_stage_events *ev);
 
 /* Same lookup for CALLER-SUPPLIED particle states (a transport code's energies and materials):
- * E[n] in [0, 1] (finite), mat[n] in 0..11.  Device pointers, or host pointers with GF_HOST_IO.
- * macro_out [n][5|4] (may be NULL) and vsum as in gf_xs_lookup_batch. */
+ * E[n] finite (the method samples [0, 1); other finite energies follow the literal algorithm, e.g.
+ * hash bin / RS window clamped at 0), mat[n] in 0..11.  Device pointers, or host pointers with
+ * GF_HOST_IO.  macro_out [n][5|4] (may be NULL) and vsum as in gf_xs_lookup_batch.
+ * Inputs outside that domain (mat > 11, NaN or +-inf energies) are errors.  They cannot be checked
+ * before enqueue without reading device memory, so the kernels that read the inputs flag them: bit 63
+ * of *vsum is set (a valid raw sum is < 2^63) and gf_xs_verify returns GF_E_INVAL for such a sum; the
+ * other lookups' results are still computed and the flagged ones' outputs are unspecified.  With
+ * GF_HOST_IO the call completes before returning and returns GF_E_INVAL itself (*vsum untouched). */
 gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint8_t *mat, uint64_t n, uint32_t flags,
                                 double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
                                 gf_stream_t stream);
@@ -224,9 +237,17 @@ gf_status gf_xs_grid_info(const gf_xs_grid *g, int32_t *fastdiv);
  * index grid / warp search (0).  Every choice gives bit-identical results.  Not synchronised with
  * lookups in flight on the same grid: call it between batches.  GF_E_INVAL for an unknown kernel or
  * an RSBench grid. */
-enum { GF_KERN_AUTO = 0, GF_KERN_GROUP = 1, GF_KERN_THREAD = 2, GF_KERN_STAGED = 3, GF_KERN_TILE = 4,
+enum { GF_KERN_AUTO = 0, GF_KERN_GROUP = 1, GF_KERN_THREAD = 2, /* 3 retired */ GF_KERN_TILE = 4,
        GF_KERN_TILE_NB = 5, GF_KERN_WARP_SEARCH = 6 };
 gf_status gf_xs_debug_set_kernel(gf_xs_grid *g, int32_t kern, uint64_t tile_min, int32_t nb_on);
+/* Test hook: ieee = 1 makes the lookup kernels of this grid divide with IEEE __ddiv_rn (the path grids
+ * with a zero-width interval take) instead of the exact reciprocal scheme; ieee = 0 restores the
+ * grid's own choice.  Results are bit-identical either way (both give the RN quotient). */
+gf_status gf_xs_debug_set_division(gf_xs_grid *g, int32_t ieee);
+/* The sorted-path kernel (GF_KERN_*) a batch of n lookups with `flags` runs on this grid (the nuclide
+ * grid reports GF_KERN_THREAD for its NB-bracket kernel); -1 for RSBench grids and unsorted batches,
+ * which have one kernel each.  For reports (bench) and tests. */
+gf_status gf_xs_kernel_for(const gf_xs_grid *g, uint64_t n, uint32_t flags, int32_t *kern);
 
 /* Diagnostics: d_out[i] = the lookup kernels' reciprocal division of d_a[i] by d_b[i] (device
  * arrays of n doubles), d_ref[i] = IEEE a / b (__ddiv_rn).  The two must agree bit for bit for
@@ -235,7 +256,9 @@ gf_status gf_xs_selftest_div(const double *d_a, const double *d_b, double *d_out
                              gf_stream_t stream);
 
 /* Host-only finalisation: *hash = raw_sum % 999983 (R-MOD: once, after all batches and shards).
- * If expected != UINT64_MAX and *hash != expected, returns GF_E_MISMATCH (hash still written). */
+ * If expected != UINT64_MAX and *hash != expected, returns GF_E_MISMATCH (hash still written).
+ * A raw sum with bit 63 set carries the invalid-input flag of gf_xs_lookup_energies: GF_E_INVAL,
+ * *hash not written. */
 gf_status gf_xs_verify(uint64_t raw_sum, uint64_t expected, uint64_t *hash);
 
 /* Thread-local text for the last non-OK status returned on this thread ("" if none). */

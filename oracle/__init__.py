@@ -262,6 +262,8 @@ class XSOracle:
         mat = np.ascontiguousarray(mat, dtype=np.int32)
         out = np.zeros((len(E), 5), dtype=np.float64)
         raw = lib().xso_lookup_energies(self.h, _ptr(E), _ptr(mat), len(E), _ptr(out))
+        if raw == (1 << 64) - 1:
+            raise ValueError("invalid caller inputs: material ids must be 0..11 and energies finite")
         return raw, out
 
 

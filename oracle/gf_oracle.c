@@ -404,8 +404,13 @@ uint64_t xso_lookup_indices(const xs_oracle *o, const uint64_t *idx, uint64_t n,
     return raw;
 }
 
-/* Caller-supplied (E, mat) pairs (the energies entry point). */
+/* Caller-supplied (E, mat) pairs (the energies entry point).  Input domain (DESIGN.md Sec. 3,
+ * "caller energies"): a material id in 0..11 (the 12 Hoogenboom-Martin materials, SURVEY.md:552) and a
+ * finite energy; anything else is rejected as a whole with UINT64_MAX (errors as values),
+ * before any lookup runs. */
 uint64_t xso_lookup_energies(const xs_oracle *o, const double *E, const int *mat, uint64_t n, double *macro_out) {
+    for (uint64_t t = 0; t < n; t++)
+        if (mat[t] < 0 || mat[t] >= 12 || !isfinite(E[t])) return UINT64_MAX;
     uint64_t raw = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(+ : raw)
     for (long long t = 0; t < (long long)n; t++) {

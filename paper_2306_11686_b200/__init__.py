@@ -85,6 +85,7 @@ def lib():
             "gf_xs_grid_free": (i32, [vp]),
             "gf_xs_grid_array": (i32, [vp, i32, P(vp), P(sz), P(C.c_int64)]),
             "gf_xs_batch_bytes": (i32, [vp, u64, C.c_uint32, P(sz)]),
+            "gf_xs_batch_bytes_whole": (i32, [vp, u64, C.c_uint32, P(sz)]),
             "gf_xs_lookup_batch": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_lookup_batch_ev": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp, vp]),
             "gf_xs_lookup_energies": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, vp, sz, vp]),
@@ -93,6 +94,8 @@ def lib():
             "gf_xs_verify": (i32, [u64, u64, P(u64)]),
             "gf_xs_grid_info": (i32, [vp, P(i32)]),
             "gf_xs_debug_set_kernel": (i32, [vp, i32, u64, i32]),
+            "gf_xs_kernel_for": (i32, [vp, u64, C.c_uint32, P(i32)]),
+            "gf_xs_debug_set_division": (i32, [vp, i32]),
             "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
             "gf_xs_last_error": (C.c_char_p, []),
             "gf_pr_graph_bytes": (i32, [C.c_int64, i32, P(sz), P(sz)]),
@@ -122,9 +125,11 @@ def _check(status: int):
 
 
 def verify(raw: int, expected: int | None = None) -> int:
-    """hash = raw % 999983 (once, after all batches and shards: R-MOD)."""
+    """hash = raw % 999983 (once, after all batches and shards: R-MOD).  Raises GFError(GF_E_INVAL)
+    for a raw sum carrying the invalid-input flag (bit 63; gf_xs_lookup_energies)."""
     h = C.c_uint64()
-    st = lib().gf_xs_verify(int(raw), (1 << 64) - 1 if expected is None else int(expected), C.byref(h))
+    st = lib().gf_xs_verify(int(raw) & ((1 << 64) - 1), (1 << 64) - 1 if expected is None else int(expected),
+                            C.byref(h))
     if st not in (0, 5):
         _check(st)
     if st == 5:
@@ -190,7 +195,7 @@ class Grid:
         self.h = h
         self.bench = params.bench
         self.channels = 5 if params.bench == XSBENCH else 4
-        self._scratch = None
+        self._scratch = {}  # one scratch buffer per CUDA stream (async calls on different streams must not share)
 
     @property
     def fastdiv(self) -> bool:
@@ -198,11 +203,21 @@ class Grid:
         _check(lib().gf_xs_grid_info(self.h, C.byref(v)))
         return bool(v.value)
 
-    KERNELS = {"auto": 0, "group": 1, "thread": 2, "staged": 3, "tile": 4, "tilenb": 5, "warp": 6}
+    KERNELS = {"auto": 0, "group": 1, "thread": 2, "tile": 4, "tilenb": 5, "warp": 6}
 
     def set_kernel(self, kern: str = "auto", tile_min: int = 0, nb: bool = True):
         """A/B and test hook (gf_xs_debug_set_kernel): force the sorted-path kernel of this grid."""
         _check(lib().gf_xs_debug_set_kernel(self.h, self.KERNELS[kern], tile_min, 1 if nb else 0))
+
+    def set_ieee_division(self, ieee: bool = True):
+        """Test hook (gf_xs_debug_set_division): IEEE __ddiv_rn instead of the exact reciprocal scheme."""
+        _check(lib().gf_xs_debug_set_division(self.h, 1 if ieee else 0))
+
+    def kernel_for(self, n: int, flags: int = SORT_LOCALITY) -> str:
+        """Name of the sorted-path kernel a batch of n lookups runs (gf_xs_kernel_for); "" if one kernel only."""
+        k = C.c_int32()
+        _check(lib().gf_xs_kernel_for(self.h, n, flags, C.byref(k)))
+        return {v: name for name, v in self.KERNELS.items()}.get(k.value, "")
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:
@@ -236,22 +251,31 @@ class Grid:
         return t, pitch.value
 
     # ----------------------------------------------------------------- lookups
-    def scratch_bytes(self, n: int, flags: int) -> int:
+    def scratch_bytes(self, n: int, flags: int, whole: bool = False) -> int:
+        """gf_xs_batch_bytes; whole=True: the larger size of the whole-batch host-I/O mode
+        (gf_xs_batch_bytes_whole; host-I/O energies without per-lookup outputs)."""
         b = C.c_size_t()
-        _check(lib().gf_xs_batch_bytes(self.h, n, flags, C.byref(b)))
+        _check((lib().gf_xs_batch_bytes_whole if whole else lib().gf_xs_batch_bytes)(self.h, n, flags, C.byref(b)))
         return b.value
 
-    def _get_scratch(self, n: int, flags: int):
-        need = self.scratch_bytes(n, flags)
-        if self._scratch is None or self._scratch.numel() < need:
-            self._scratch = self.torch.empty(need, dtype=self.torch.uint8, device=self.device)
-        return self._scratch
+    def _get_scratch(self, need: int, stream=None):
+        """The scratch buffer of `stream` (default: the current stream), grown to `need` bytes.  It is
+        allocated on that stream, so the caching allocator reuses a replaced buffer only for work
+        ordered after it on the same stream."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        buf = self._scratch.get(s.cuda_stream)
+        if buf is None or buf.numel() < need:
+            with torch.cuda.stream(s):
+                buf = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self._scratch[s.cuda_stream] = buf
+        return buf
 
     def lookup_batch_async(self, first: int, n: int, vsum, seed: int = STARTING_SEED, sort: bool = True,
                            macro_out=None, stream=None):
         """Enqueue lookups [first, first+n); ADDS sum(1+argmax) to the int64 device tensor `vsum`."""
         flags = SORT_LOCALITY if sort else 0
-        sc = self._get_scratch(n, flags)
+        sc = self._get_scratch(self.scratch_bytes(n, flags), stream)
         st = _stream_ptr(self.torch, stream)
         mo = C.c_void_p(macro_out.data_ptr()) if macro_out is not None else None
         _check(lib().gf_xs_lookup_batch(self.h, first, n, seed, flags, mo, C.c_void_p(vsum.data_ptr()),
@@ -267,17 +291,44 @@ class Grid:
         raw = int(vsum.item())
         return (raw, macro) if want_macro else raw
 
-    def lookup_energies(self, E, mat, sort: bool = True, want_macro: bool = True, stream=None, out=None):
-        """Caller-supplied states.  Device tensors -> device outputs; pinned/CPU tensors -> the call
-        stages them (GF_HOST_IO, pipelined H2D / lookup / D2H) and returns host outputs.  `out`: an
-        optional preallocated [n][5|4] fp64 output (pinned for host I/O) reused across calls."""
+    def _check_states(self, E, mat, out, want_macro):
+        """Argument checks of lookup_energies (marshalling only): dtypes, contiguity, sizes and devices
+        must match what gf_xs_lookup_energies reads and writes, else ValueError (never a raw pointer
+        into a wrong-sized or wrong-typed buffer)."""
         torch = self.torch
+        if not isinstance(E, torch.Tensor) or not isinstance(mat, torch.Tensor):
+            raise ValueError("E and mat must be torch tensors")
+        if E.dtype != torch.float64 or mat.dtype != torch.uint8:
+            raise ValueError(f"E must be float64 and mat uint8 (got {E.dtype}, {mat.dtype})")
+        if E.dim() != 1 or mat.dim() != 1 or E.numel() != mat.numel():
+            raise ValueError(f"E and mat must be 1-D of equal length (got {tuple(E.shape)}, {tuple(mat.shape)})")
+        if not E.is_contiguous() or not mat.is_contiguous():
+            raise ValueError("E and mat must be contiguous")
+        if E.device != mat.device:
+            raise ValueError(f"E and mat must be on the same device (got {E.device}, {mat.device})")
+        if E.is_cuda and E.device != self.device:
+            raise ValueError(f"device tensors must be on the grid's device {self.device} (got {E.device})")
+        if out is not None:
+            if not want_macro:
+                raise ValueError("out given with want_macro=False")
+            if (out.dtype != torch.float64 or tuple(out.shape) != (E.numel(), self.channels)
+                    or not out.is_contiguous() or out.device != E.device):
+                raise ValueError(f"out must be a contiguous float64 [{E.numel()}][{self.channels}] tensor on {E.device}")
+
+    def lookup_energies(self, E, mat, sort: bool = True, want_macro: bool = True, stream=None, out=None):
+        """Caller-supplied states (E float64 [n], mat uint8 [n]).  Device tensors -> device outputs;
+        CPU tensors (pinned for speed) -> the call stages them (GF_HOST_IO, pipelined H2D / lookup /
+        D2H) and returns host outputs.  `out`: an optional preallocated [n][5|4] fp64 output (pinned
+        for host I/O) reused across calls.  Material ids > 11 or non-finite energies raise GFError
+        (GF_E_INVAL; include/gf_xs.h)."""
+        torch = self.torch
+        self._check_states(E, mat, out, want_macro)
         n = E.numel()
         host = not E.is_cuda
         flags = (SORT_LOCALITY if sort else 0) | (HOST_IO if host else 0)
-        sc = self._get_scratch(n, flags)
         st = _stream_ptr(torch, stream)
         if host:
+            sc = self._get_scratch(self.scratch_bytes(n, flags, whole=not want_macro), stream)
             vs = C.c_uint64(0)
             macro = out
             if want_macro and macro is None:
@@ -286,12 +337,17 @@ class Grid:
                                                C.c_void_p(macro.data_ptr()) if want_macro else None, C.byref(vs),
                                                C.c_void_p(sc.data_ptr()), sc.numel(), st))
             return (vs.value, macro) if want_macro else vs.value
+        sc = self._get_scratch(self.scratch_bytes(n, flags), stream)
         vsum = torch.zeros(1, dtype=torch.int64, device=self.device)
-        macro = torch.empty((n, self.channels), dtype=torch.float64, device=self.device) if want_macro else None
+        macro = out
+        if want_macro and macro is None:
+            macro = torch.empty((n, self.channels), dtype=torch.float64, device=self.device)
         _check(lib().gf_xs_lookup_energies(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()), n, flags,
                                            C.c_void_p(macro.data_ptr()) if want_macro else None,
                                            C.c_void_p(vsum.data_ptr()), C.c_void_p(sc.data_ptr()), sc.numel(), st))
         raw = int(vsum.item())
+        if raw < 0:  # bit 63: the invalid-input flag
+            raise GFError(1, "invalid caller inputs: material id > 11 or non-finite energy")
         return (raw, macro) if want_macro else raw
 
     # ----------------------------------------------------------------- history mode (NEXT-1)
@@ -305,9 +361,7 @@ class Grid:
         flags = self.HIST_MODES[mode]
         b = C.c_size_t()
         _check(lib().gf_xs_history_bytes(self.h, n_p, flags, C.byref(b)))
-        if self._scratch is None or self._scratch.numel() < b.value:
-            self._scratch = self.torch.empty(b.value, dtype=self.torch.uint8, device=self.device)
-        sc = self._scratch
+        sc = self._get_scratch(b.value, stream)
         mo = C.c_void_p(macro_out.data_ptr()) if macro_out is not None else None
         _check(lib().gf_xs_history_batch(self.h, first_p, n_p, L, seed, flags, mo, C.c_void_p(vsum.data_ptr()),
                                          C.c_void_p(sc.data_ptr()), sc.numel(), _stream_ptr(self.torch, stream)))

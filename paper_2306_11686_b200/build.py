@@ -16,8 +16,9 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libgfxs.so")
 OBJ = os.path.join(PKG, "build_obj")
 SOURCES = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
-DEPS = SOURCES + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "gf_xs.h"),
-                                                                   os.path.abspath(__file__)]
+DEPS = (SOURCES + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+        + [os.path.abspath(__file__)])
+STAMP = LIB + ".flags"  # the nvcc flags the library was built with (incl. GF_EXTRA_NVCC A/B variants)
 
 COMMON = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
           "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -32,8 +33,17 @@ def nvcc() -> str:
     return "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc"
 
 
+def _flags() -> str:
+    extra = os.environ.get("GF_EXTRA_NVCC", "")
+    return " ".join(COMMON + DEFAULT + [f"{k}:{' '.join(v)}" for k, v in sorted(PER_FILE.items())] + [extra])
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    """True if the library is missing, older than a source, or was built with other flags (e.g. an
+    A/B variant with GF_EXTRA_NVCC): a stale variant build is never silently reused."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    if open(STAMP).read() != _flags():
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(p) > t for p in DEPS)
@@ -61,6 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc link failed:\n" + res.stderr[-8000:])
     with open(os.path.join(PKG, "ptxas_report.txt"), "w") as f:
         f.write("\n".join(report))
+    with open(STAMP, "w") as f:
+        f.write(_flags())
     if verbose:
         print("\n".join(report))
     return LIB

@@ -170,7 +170,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     const size_t npts = (size_t)p->n_isotopes * (size_t)p->n_gridpoints;
     L.G = take(npts * 48);
     L.Ed = take(npts * 8);
-    L.Rd = take(npts * 8 + 16);  // +16: the staged kernel's bulk copies round ranges up to 16 B
+    L.Rd = take(npts * 8);
     L.flags = take(16);
     if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128 + 256);  // + the tile kernel's slot overrun
     if (p->grid_type == GF_GRID_NUCLIDE && p->n_gridpoints < 65536) {  // sorted batches search NB brackets
@@ -224,7 +224,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
 
 // Sorted-path kernel choice, read once per grid here (never on the lookup path).  The environment
 // overrides exist for A/B measurements only; every choice gives identical results.
-//   GF_XS_KERNEL   = tile | tilenb | group | thread | staged | warp   (default: auto)
+//   GF_XS_KERNEL   = tile | tilenb | group | thread | warp   (default: auto)
 //   GF_XS_TILE_MIN = smallest batch of the warp-tile kernel in auto mode (default kTileMinN)
 //   GF_XS_GROUP_MIN = smallest batch of the group kernel in auto mode (default kGroupMinN)
 //   GF_XS_NB       = 0: sparse batches search the index grid instead of the NB brackets
@@ -239,7 +239,6 @@ static void kernel_choice(XsDev &X) {
     else if (v == "tilenb") X.kern = kKernTileNB;
     else if (v == "group") X.kern = kKernGroup;
     else if (v == "thread") X.kern = kKernThread;
-    else if (v == "staged") X.kern = kKernStaged;
     else if (v == "warp") X.kern = kKernWarpSearch;
   }
   X.tile_min = kTileMinN;
@@ -259,6 +258,7 @@ struct ArrView {
 
 struct gf_xs_grid {
   gf_xs_params p;
+  int fastdiv_ok = 0;  // the grid admits the exact reciprocal division (no zero-width interval)
   int device = 0;
   int total = 0;
   XsDev xs{};
@@ -447,6 +447,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       if (ce == cudaSuccess) ce = cudaMemcpyAsync(&zw, zero_width, sizeof(int), cudaMemcpyDeviceToHost, st);
       if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
       X.fastdiv = (zw == 0) ? 1 : 0;
+      g->fastdiv_ok = X.fastdiv;
     } else if (ce == cudaSuccess) {
       RsDev &R = g->rs;
       const int n = p->n_isotopes;
@@ -509,7 +510,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, tinfo, work, h_macro, h_E, h_mat, bytes;
+  size_t counts, cursor, btot, mstart, Es, idx, us, work, h_macro, h_E, h_mat, bytes;
 };
 struct BatchLayout {
   SlotLayout slot;
@@ -522,15 +523,17 @@ struct BatchLayout {
 static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want_macro, bool energies,
                       SlotLayout &L);
 
+// whole: plan the whole-batch host-I/O slot too (host-I/O energies, sorted, no per-lookup outputs);
+// otherwise the chunked pipeline's two chunk slots only, whose size is bounded by the chunk.
 static void plan_batch(const gf_xs_grid *g, uint64_t n, uint32_t flags, bool want_macro, bool energies,
-                       BatchLayout &B) {
+                       BatchLayout &B, bool whole = false) {
   memset(&B, 0, sizeof B);
   const bool host_io = (flags & GF_HOST_IO) != 0;
   const uint64_t m = host_io ? (n < kIoChunk ? n : kIoChunk) : n;
   plan_slot(g, m, flags, want_macro, energies, B.slot);
   B.slots = host_io ? 2 : 1;
   size_t end = B.slots * B.slot.bytes;
-  if (host_io && energies && (flags & GF_SORT_LOCALITY)) {
+  if (whole && host_io && energies && !want_macro && (flags & GF_SORT_LOCALITY)) {
     plan_slot(g, n, flags, false, true, B.full);
     B.has_full = true;
     end = std::max(end, B.full.bytes);
@@ -557,7 +560,6 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
     L.Es = take(sizeof(double) * m);
     L.idx = take(sizeof(uint32_t) * m);
     L.us = take(sizeof(uint32_t) * m);
-    L.tinfo = take(32 * ((m + 127) / 128));
     L.work = take(256);
   }
   if (host_io) {
@@ -573,8 +575,17 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
 gf_status gf_xs_batch_bytes(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes) {
   if (!g || !scratch_bytes) return fail(GF_E_INVAL, "grid or scratch_bytes is NULL");
   BatchLayout B;
-  plan_batch(g, n_lookups, flags, true, true, B);  // upper bound over the optional parts
+  plan_batch(g, n_lookups, flags, true, true, B);  // upper bound over the optional parts (chunked host I/O)
   *scratch_bytes = B.total;
+  return GF_OK;
+}
+
+gf_status gf_xs_batch_bytes_whole(const gf_xs_grid *g, uint64_t n_lookups, uint32_t flags, size_t *scratch_bytes) {
+  if (!g || !scratch_bytes) return fail(GF_E_INVAL, "grid or scratch_bytes is NULL");
+  BatchLayout Bc, Bw;
+  plan_batch(g, n_lookups, flags, true, true, Bc);
+  plan_batch(g, n_lookups, flags, false, true, Bw, true);
+  *scratch_bytes = std::max(Bc.total, Bw.total);
   return GF_OK;
 }
 
@@ -587,7 +598,6 @@ static SortScratch slot_sort(char *base, const SlotLayout &L) {
   S.Es = reinterpret_cast<double *>(base + L.Es);
   S.idx = reinterpret_cast<uint32_t *>(base + L.idx);
   S.us = reinterpret_cast<uint32_t *>(base + L.us);
-  S.tinfo = base + L.tinfo;
   S.work = reinterpret_cast<uint32_t *>(base + L.work);
   return S;
 }
@@ -642,7 +652,7 @@ static gf_status run_host_io(const gf_xs_grid *gc, uint64_t first, uint64_t n, u
       GF_CUDA(cudaMemcpyAsync(dmat + off, mat + off, cn, cudaMemcpyHostToDevice, sin));
       GF_CUDA(cudaEventRecord(h2d[0], sin));
       GF_CUDA(cudaStreamWaitEvent(scomp, h2d[0], 0));
-      ce = launch_sort_count((uint32_t)n, (uint32_t)cn, dE + off, dmat + off, thr, S, scomp);
+      ce = launch_sort_count((uint32_t)n, (uint32_t)cn, dE + off, dmat + off, thr, S, dvsum, scomp);
       if (ce != cudaSuccess) return fail(GF_E_CUDA, "sort count: %s", cudaGetErrorString(ce));
     }
     ce = launch_lookup(g, first, (uint32_t)n, seed, dE, dmat, true, S, nullptr, dvsum, scomp, nullptr);
@@ -650,6 +660,7 @@ static gf_status run_host_io(const gf_xs_grid *gc, uint64_t first, uint64_t n, u
     uint64_t add = 0;
     GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, scomp));
     GF_CUDA(cudaStreamSynchronize(scomp));
+    if (add & kInvalidInputBit) return fail(GF_E_INVAL, "invalid caller inputs: material id > 11 or non-finite energy");
     *vsum += add;
     return GF_OK;
   }
@@ -684,6 +695,7 @@ static gf_status run_host_io(const gf_xs_grid *gc, uint64_t first, uint64_t n, u
   GF_CUDA(cudaMemcpyAsync(&add, dvsum, 8, cudaMemcpyDeviceToHost, scomp));
   GF_CUDA(cudaStreamSynchronize(scomp));
   GF_CUDA(cudaStreamSynchronize(sout));
+  if (add & kInvalidInputBit) return fail(GF_E_INVAL, "invalid caller inputs: material id > 11 or non-finite energy");
   *vsum += add;
   return GF_OK;
 }
@@ -702,7 +714,9 @@ static gf_status run_lookup(const gf_xs_grid *g, uint64_t first, uint64_t n, uin
     return fail(GF_E_UNSUPPORTED, "energy-band grids serve sorted, device-resident event lookups only");
   const bool host_io = (flags & GF_HOST_IO) != 0;
   BatchLayout B;
-  plan_batch(g, n, flags, macro_out != nullptr, energies, B);
+  plan_batch(g, n, flags, macro_out != nullptr, energies, B, true);  // the whole-batch host-I/O mode if it fits,
+  if (B.has_full && scratch_bytes < B.total)                        // else the chunked pipeline
+    plan_batch(g, n, flags, macro_out != nullptr, energies, B, false);
   if (n && (!scratch || scratch_bytes < B.total))
     return fail(GF_E_NOMEM, "scratch %zu B < required %zu B", scratch_bytes, B.total);
   if (n && ((uintptr_t)scratch & 255)) return fail(GF_E_INVAL, "scratch must be 256-byte aligned");
@@ -869,11 +883,32 @@ gf_status gf_xs_selftest_div(const double *d_a, const double *d_b, double *d_out
 gf_status gf_xs_debug_set_kernel(gf_xs_grid *g, int32_t kern, uint64_t tile_min, int32_t nb_on) {
   if (!g) return fail(GF_E_INVAL, "grid is NULL");
   if (g->p.bench != GF_XSBENCH) return fail(GF_E_INVAL, "kernel choice applies to XSBench grids");
-  if (kern < GF_KERN_AUTO || kern > GF_KERN_WARP_SEARCH) return fail(GF_E_INVAL, "unknown kernel %d", kern);
+  if (kern < GF_KERN_AUTO || kern > GF_KERN_WARP_SEARCH || kern == 3) return fail(GF_E_INVAL, "unknown kernel %d", kern);
   if (tile_min >= (1ull << 32)) return fail(GF_E_INVAL, "tile_min %llu >= 2^32", (unsigned long long)tile_min);
   g->xs.kern = kern;
   if (tile_min) g->xs.tile_min = (uint32_t)tile_min;
   g->xs.nb_on = nb_on ? 1 : 0;
+  return GF_OK;
+}
+
+gf_status gf_xs_debug_set_division(gf_xs_grid *g, int32_t ieee) {
+  if (!g) return fail(GF_E_INVAL, "grid is NULL");
+  if (g->p.bench != GF_XSBENCH) return fail(GF_E_INVAL, "division choice applies to XSBench grids");
+  g->xs.fastdiv = ieee ? 0 : g->fastdiv_ok;
+  return GF_OK;
+}
+
+gf_status gf_xs_kernel_for(const gf_xs_grid *g, uint64_t n, uint32_t flags, int32_t *kern) {
+  if (!g || !kern) return fail(GF_E_INVAL, "grid or kern is NULL");
+  *kern = -1;
+  if (g->p.bench != GF_XSBENCH || !(flags & GF_SORT_LOCALITY)) return GF_OK;  // RS / unsorted: one kernel each
+  const XsDev &X = g->xs;
+  if (X.grid_type == GF_GRID_NUCLIDE) {
+    *kern = (X.NB && X.nb_on && X.kern != kKernWarpSearch) ? GF_KERN_THREAD
+            : (X.kern == kKernThread ? GF_KERN_THREAD : GF_KERN_WARP_SEARCH);
+    return GF_OK;
+  }
+  *kern = X.kern != kKernAuto ? X.kern : (n >= X.tile_min ? GF_KERN_TILE : n >= X.group_min ? GF_KERN_GROUP : GF_KERN_THREAD);
   return GF_OK;
 }
 
@@ -885,6 +920,9 @@ gf_status gf_xs_grid_info(const gf_xs_grid *g, int32_t *fastdiv) {
 
 gf_status gf_xs_verify(uint64_t raw_sum, uint64_t expected, uint64_t *hash) {
   if (!hash) return fail(GF_E_INVAL, "hash is NULL");
+  if (raw_sum & kInvalidInputBit)
+    return fail(GF_E_INVAL, "raw sum carries the invalid-input flag (bit 63): a caller lookup had a material "
+                "id > 11 or a non-finite energy");
   *hash = raw_sum % GF_HASH_MODULUS;
   if (expected != UINT64_MAX && *hash != expected)
     return fail(GF_E_MISMATCH, "hash %llu != expected %llu", (unsigned long long)*hash, (unsigned long long)expected);

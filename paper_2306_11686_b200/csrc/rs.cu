@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kRsTpb) rs_lookup_direct(RsDev R, uint64_t fir
     if (src_E) {
       E = src_E[t];
       mat = src_mat[t];
+      if (mat >= kMats || !isfinite(E)) invalid_input(vsum);
       mat = mat < kMats ? mat : kMats - 1;
     } else {
       uint64_t s = lcg_skip(seed, 2ull * (first + t));
@@ -361,7 +362,7 @@ cudaError_t launch_rs_lookup(const RsDev &R, uint64_t first, uint32_t n, uint64_
   const size_t smem = table_smem(R.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, R.thr, S, out.any(), st)) != cudaSuccess)
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, R.thr, S, out.any(), vsum, st)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
     if ((e = allow_smem(rs_lookup_sorted, smem)) != cudaSuccess) return e;

@@ -17,9 +17,6 @@
 
 namespace gf {
 
-#ifndef GF_DIAG_SCATTER
-#define GF_DIAG_SCATTER 0
-#endif
 constexpr int kRun = 16;   // sort_scatter: lookups per thread (registers hold them between phases)
 constexpr int kRunC = 16;  // sort_count: lookups per thread (64 measured: no faster at 17 M, slower for small batches)
 
@@ -40,7 +37,8 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
-                                                  double band_lo, double band_hi, int nb_log2) {
+                                                  double band_lo, double band_hi, int nb_log2,
+                                                  unsigned long long *__restrict__ flag) {
   __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
   if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   __syncthreads();
@@ -56,6 +54,7 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
     if (src_E) {
       E = src_E[t];
       mat = src_mat[t];
+      if (mat >= kMats || !isfinite(E)) invalid_input(flag);  // outside the input domain: flagged
       mat = mat < kMats ? mat : kMats - 1;
     } else {
       E = lcg_draw(s);
@@ -154,21 +153,12 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
                                                : 0xFFFFFFFFu;
     }
   }
-#if GF_DIAG_SCATTER == 1  // diagnostic (wrong results): stores at a hash position, no atomics
-#pragma unroll
-  for (int r = 0; r < kRun; r++)
-    if (r < cnt) pos[r] = (uint32_t)(((t0 + r) * 2654435761ull) % n);
-#else
 #pragma unroll
   for (int r = 0; r < kRun; r++)
     if (r < cnt && pos[r] != 0xFFFFFFFFu) pos[r] = atomicAdd(cursor + pos[r], 1u);
-#endif
 #pragma unroll
   for (int r = 0; r < kRun; r++) {
     if (r < cnt && pos[r] != 0xFFFFFFFFu) {  // (outside the band: dropped)
-#if GF_DIAG_SCATTER == 2  // diagnostic (wrong results): atomics only, no stores
-      if (E[r] < -1.0)
-#endif
       Es[pos[r]] = E[r];
       if (idx) idx[pos[r]] = (uint32_t)(t0 + r);
     }
@@ -197,16 +187,16 @@ cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) 
 // Counts caller lookups [0, cn) of a chunk (src_E / src_mat point at the chunk) into the bins of an
 // n_total-lookup batch (no band grids: the host-IO path rejects them).
 cudaError_t launch_sort_count(uint32_t n_total, uint32_t cn, const double *src_E, const uint8_t *src_mat,
-                              const double *thr, const SortScratch &S, cudaStream_t st) {
+                              const double *thr, const SortScratch &S, unsigned long long *flag, cudaStream_t st) {
   const double inf = HUGE_VAL;
   const unsigned gc = nblk(((long long)cn + kRunC - 1) / kRunC, 256);
-  sort_count<<<gc, 256, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, sort_bits(n_total));
+  sort_count<<<gc, 256, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, sort_bits(n_total), flag);
   return cudaGetLastError();
 }
 
 cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
-                                 cudaStream_t st, double band_lo, double band_hi) {
+                                 unsigned long long *flag, cudaStream_t st, double band_lo, double band_hi) {
   cudaError_t e;
   const int nbl = sort_bits(n);
   const int bins = kMats << nbl;  // a multiple of kScanBlk for nbl >= 10
@@ -214,7 +204,7 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
   if (!S.counted) {
     if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
     const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, 256);
-    sort_count<<<gc, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl);
+    sort_count<<<gc, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);

@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kLookupTpb) xs_lookup_direct(XsDev X, uint64_t
     if (src_E) {
       E = src_E[t];
       mat = src_mat[t];
+      if (mat >= kMats || !isfinite(E)) invalid_input(vsum);
       mat = mat < kMats ? mat : kMats - 1;
     } else {
       uint64_t s = lcg_skip(seed, 2ull * (first + t));
@@ -387,9 +388,6 @@ __global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(X
   hash_epilogue(v, vsum);
 }
 
-// ------------------------------------------------------------------------------------------ staged
-#include "xs_staged.cuh"
-
 // ------------------------------------------------------------------------------------------ production
 #include "xs_sorted_u.cuh"
 #include "xs_warp_nuclide.cuh"
@@ -403,8 +401,7 @@ __global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(X
 // staged records (measured).  The nuclide grid searches the
 // per-nuclide bin brackets (NB).  The alternatives stay selectable for A/B measurements
 // (GF_XS_KERNEL at grid init): group (4 lookups per thread, per-lookup index-grid loads), thread,
-// staged (TMA producer / consumer ring, unionized), tilenb (tile runs from the NB brackets), warp
-// (warp-cooperative nuclide-grid search).
+// tilenb (tile runs from the NB brackets), warp (warp-cooperative nuclide-grid search).
 static int sorted_kernel(const XsDev &X, uint32_t n) {
   if (X.kern != kKernAuto) return X.kern;
   return n >= X.tile_min ? kKernTile : n >= X.group_min ? kKernGroup : kKernThread;
@@ -417,14 +414,11 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
   const size_t smem = xs_table_smem(X.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), st, X.band_lo, X.band_hi)) !=
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), vsum, st, X.band_lo, X.band_hi)) !=
         cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
     const int kern = sorted_kernel(X, n);
-    if (GT == GF_GRID_UNIONIZED && kern == kKernStaged)
-      return X.fastdiv ? launch_staged<true>(X, n, S, out, vsum, st)
-                       : launch_staged<false>(X, n, S, out, vsum, st);
     if (GT != GF_GRID_NUCLIDE && kern == kKernGroup)
       return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
                        : launch_group<GT, false>(X, n, S, out, vsum, st);

@@ -15,8 +15,8 @@
 // persistent (grid = SMs x resident CTAs) and stage the material tables in SMEM once.  A3 runs in a separate massively parallel pass (idx_prep) so its dependent
 // search latency is not on this kernel's critical path.
 // Measured alternatives: one lookup per thread; a TMA/mbarrier producer-consumer
-// ring (xs_staged.cuh, selectable with GF_XS_KERNEL=staged); deeper register rings (instruction-cache
-// or register-file overflow).
+// ring (removed in round 2: 2x slower); deeper register rings (instruction-cache or register-file
+// overflow).
 #pragma once
 
 #ifndef GF_GROUP_L
@@ -60,10 +60,6 @@ struct Rec {
   double y;  // fast division path only
 };
 
-#ifndef GF_DIAG_NOMATH
-#define GF_DIAG_NOMATH 0  // diagnostic build only (wrong results): record consumed by 6 adds, no math
-#endif
-
 #ifndef GF_PACKTAB
 #define GF_PACKTAB 1  // group loop: record base + concentration from one 16-B shared load
 #endif
@@ -101,11 +97,6 @@ __device__ __forceinline__ void load_rec(const XsDev &X, uint32_t r, Rec &R) {
 // operations as accumulate() with the two grid-only differences read from the record.
 template <bool FAST>
 __device__ __forceinline__ void accumulate_rec(const Rec &R, double E, double conc, double m[5]) {
-#if GF_DIAG_NOMATH
-  m[0] = __dadd_rn(m[0], R.v0.x); m[1] = __dadd_rn(m[1], R.v1.y); m[2] = __dadd_rn(m[2], R.v2.y);
-  m[3] = __dadd_rn(m[3], R.v3.y); m[4] = __dadd_rn(m[4], R.v4.y); m[0] = __dadd_rn(m[0], R.v5.y + (FAST ? R.y : 0.0));
-  return;
-#endif
   const double a = __dsub_rn(R.v0.x, E), b = R.v0.y;
   const double f = FAST ? div_rn(a, b, R.y) : __ddiv_rn(a, b);
   const double2 hd[5] = {R.v1, R.v2, R.v3, R.v4, R.v5};

@@ -1,5 +1,5 @@
 // xs_tile.cuh -- the warp-tile sorted lookup kernel (A3-A6 over a locality-sorted batch; included by
-// xs_lookup.cu after xs_sorted_u.cuh and xs_staged.cuh, whose mbarrier / bulk-copy helpers it uses).
+// xs_lookup.cu after xs_sorted_u.cuh).
 //
 // A warp owns a tile of 128 consecutive sorted lookups (lane l: positions 4l .. 4l+3, sorted by energy
 // in registers).  After the locality sort a tile lies in one material and a narrow energy range
@@ -33,6 +33,32 @@ constexpr int kTileWarps = kTileTpb / 32;
 constexpr int kChunk = 10;     // nuclides per staged chunk (lanes 0..9 stage one each; 4 CTAs fit an SM)
 constexpr int kRecs = 4;       // interval records staged per (tile, nuclide): klo .. klo + 3
 constexpr int kSlotBytes = 128 * kRecs;
+
+// mbarrier / bulk-copy (TMA 1-D) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 struct TileSmem {  // per warp
   unsigned char rec[2][kChunk][kSlotBytes];  // [buffer][slot]: records klo .. klo + kRecs - 1

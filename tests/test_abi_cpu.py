@@ -60,6 +60,20 @@ def test_no_fma_contraction_in_xs_lookup_sass():
     assert checked >= 6
 
 
+def test_verify_rejects_invalid_input_flag():
+    """Bit 63 of a raw sum is the device-side invalid-input flag of gf_xs_lookup_energies (include/gf_xs.h):
+    gf_xs_verify returns GF_E_INVAL for it; a valid raw sum (< 2^63) is untouched."""
+    import ctypes as C
+    h = C.c_uint64(7)
+    assert gf.lib().gf_xs_verify((1 << 63) | 51112661, (1 << 64) - 1, C.byref(h)) == 1
+    assert h.value == 7  # not written
+    assert "invalid-input" in gf.lib().gf_xs_last_error().decode()
+    with pytest.raises(gf.GFError) as e:
+        gf.verify((1 << 63) | 5)
+    assert e.value.status == 1
+    assert gf.verify((1 << 63) - 1) == ((1 << 63) - 1) % 999983
+
+
 def test_version_and_verify():
     assert b"sm_100a" in gf.lib().gf_xs_version()
     assert gf.verify(51112661) == 113528
@@ -98,7 +112,7 @@ def test_grid_bytes_closed_form():
             want += al(npts * 8) + al(n_iso * pitch * 2) + al((2 ** 20 + 1) * 4)
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts (sparse batches)
         if gt != gf.NUCLIDE:
-            want += al(npts * 128)  # interval records of the sorted kernel
+            want += al(npts * 128 + 256)  # interval records of the sorted kernels (+ 2 records of tile-slot overrun)
         else:
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts
         if gt == gf.HASH:

@@ -47,7 +47,16 @@ def test_gloo_sharded_hash_equals_single_process(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    raw, h, t = q.get(timeout=300)
+    import queue
+    import time
+    deadline = time.time() + 300
+    while True:  # fail fast if a worker dies instead of waiting for the queue
+        try:
+            raw, h, t = q.get(timeout=2)
+            break
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead and time.time() < deadline, f"gloo workers failed: exit codes {dead}"
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -58,7 +67,7 @@ def test_gloo_sharded_hash_equals_single_process(world):
 
 
 def test_weak_ranges_tile_the_batch():
-    """Weak scaling (bench default): rank r of W runs [r n, (r+1) n); the ranges tile [0, W n), so the
+    """Weak scaling (bench --scaling weak): rank r of W runs [r n, (r+1) n); the ranges tile [0, W n), so the
     all-reduced raw sum of W ranks is the raw sum of one W n batch (hash additivity)."""
     import oracle as O
     import paper_2306_11686_b200 as gf

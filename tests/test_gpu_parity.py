@@ -150,7 +150,7 @@ def test_n_zero_and_flags(gf, torch):
     v = torch.zeros(1, dtype=torch.int64, device="cuda")
     with pytest.raises(gf.GFError) as e:
         import ctypes as C
-        sc = g._get_scratch(10, 0)
+        sc = g._get_scratch(g.scratch_bytes(10, 0))
         gf._check(gf.lib().gf_xs_lookup_batch(g.h, 0, 10, 1070, gf.HISTORY, None, C.c_void_p(v.data_ptr()),
                                               C.c_void_p(sc.data_ptr()), sc.numel(), None))
     assert e.value.status == 4
@@ -217,11 +217,10 @@ def test_C2_small_unionized(gf):
     assert raw == golden()["C2"]["raw"] and gf.verify(raw) == golden()["C2"]["hash"]
 
 
-@pytest.mark.parametrize("kernel,grid", [("staged", 1), ("thread", 1), ("group", 1), ("tile", 1), ("tilenb", 1),
+@pytest.mark.parametrize("kernel,grid", [("thread", 1), ("group", 1), ("tile", 1), ("tilenb", 1),
                                          ("thread", 0), ("warp", 0), ("group", 2), ("tile", 2)])
 def test_alternative_sorted_kernels_match(gf, kernel, grid):
-    """gf_xs_debug_set_kernel forces one kernel of the sorted path for every batch size (the TMA-staged
-    producer/consumer ring, the per-thread kernel, the 4-lookups-per-thread group kernel, the warp-tile
+    """gf_xs_debug_set_kernel forces one kernel of the sorted path for every batch size (the per-thread kernel, the 4-lookups-per-thread group kernel, the warp-tile
     kernel with index-grid or NB runs, the warp-cooperative nuclide search); each must give the
     oracle's bits.  At 200 k lookups a tile spans many intervals per nuclide, so the tile kernel's
     runs overflow kNbMax and its per-lookup search fallback runs too."""
@@ -364,11 +363,11 @@ def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
 
 
 def test_nuclide_warp_search_edges(gf, torch):
-    """The nuclide-grid sorted kernel searches once per warp (32-ary warp-cooperative search over the
-    warp's [Emin, Emax], then a shuffle search per lane).  Exact gridpoints and their 1-ulp
-    neighbours inside one warp, dense clusters (narrow warps), a sparse spread (wide warps that end
-    in the per-lane fallback), the grid ends, energies outside [0, 1], +-inf and NaN (which takes
-    grid_search's per-lane path) must all give the oracle's bits."""
+    """The nuclide-grid sorted kernels: the warp-cooperative search (once per warp, 32-ary over the
+    warp's [Emin, Emax], then a shuffle search per lane) and the NB-bracket kernel (auto).  Exact
+    gridpoints and their 1-ulp neighbours inside one warp, dense clusters (narrow warps), a sparse
+    spread (wide warps that end in the per-lane fallback), the grid ends, energies outside [0, 1],
+    -0.0 and subnormals must all give the oracle's bits."""
     o, g = make_pair(gf, 68, 11303, O.NUCLIDE)
     rng = np.random.default_rng(5)
     G = o.nuclide_grid()
@@ -379,19 +378,43 @@ def test_nuclide_warp_search_edges(gf, torch):
             Es += [e, math.nextafter(e, -1), math.nextafter(e, 2), e] + list(e + (rng.random(12) - 0.5) * 1e-6)
     Es += list(0.25 + rng.random(3000) * 1e-4)            # narrow warps
     Es += list(rng.random(40))                             # wide warps
-    Es += [0.0, 1.0, -0.5, 3.0, math.inf, -math.inf, 5e-324, -0.0]
+    Es += [0.0, 1.0, -0.5, 3.0, 1e300, -1e300, 5e-324, -0.0]
     E = np.array(Es)
     for kern, mat in [("warp", 0), ("warp", 4), ("warp", 7), ("auto", 0), ("auto", 7)]:  # auto: NB brackets
         g.set_kernel(kern)
-        for extra in ([], [math.nan, math.nan, 0.5]):
-            EE = np.concatenate([E, np.array(extra, dtype=np.float64)])
-            mats = np.full(len(EE), mat, dtype=np.uint8)
-            raw_o, m_o = o.lookup_energies(EE, mats.astype(np.int32))
-            raw_g, m_g = g.lookup_energies(torch.from_numpy(EE).cuda(), torch.from_numpy(mats).cuda(), sort=True)
-            m_g = m_g.cpu().numpy()
-            assert raw_g == raw_o
-            fin = ~np.isnan(m_o)
-            assert np.array_equal(np.isnan(m_g), ~fin) and np.array_equal(m_g[fin], m_o[fin]), f"mat {mat}"
+        mats = np.full(len(E), mat, dtype=np.uint8)
+        raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))
+        raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
+        assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o), (kern, mat)
+
+
+@pytest.mark.parametrize("bench,grid_type", [("xs", 0), ("xs", 1), ("xs", 2), ("rs", None)])
+def test_invalid_caller_inputs(gf, torch, bench, grid_type):
+    """Caller states outside the input domain (material id > 11, NaN, +-inf) are errors on both sides:
+    the oracle rejects the batch, the device path sets the invalid-input bit of the raw sum (the
+    binding raises GF_E_INVAL; gf_xs_verify rejects the raw), the host-I/O path returns GF_E_INVAL.
+    Valid batches around them are unaffected."""
+    g = gf.Grid(gf.Params.xsbench(68, 11303, grid_type) if bench == "xs" else gf.Params.rsbench(68))
+    rng = np.random.default_rng(3)
+    E = rng.random(5000)
+    mats = rng.integers(0, 12, 5000).astype(np.uint8)
+    ok = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), want_macro=False)
+    for bad_e, bad_m in ((math.nan, 0), (math.inf, 0), (-math.inf, 3), (0.5, 12), (0.5, 255)):
+        E2, m2 = E.copy(), mats.copy()
+        E2[1234], m2[1234] = bad_e, bad_m
+        if bench == "xs":
+            with pytest.raises(ValueError):
+                O.XSOracle(68, 11303, grid_type).lookup_energies(E2, m2.astype(np.int32))
+        for sort in (True, False):
+            with pytest.raises(gf.GFError) as e:
+                g.lookup_energies(torch.from_numpy(E2).cuda(), torch.from_numpy(m2).cuda(), sort=sort, want_macro=False)
+            assert e.value.status == 1
+        with pytest.raises(gf.GFError) as e:
+            g.lookup_energies(torch.from_numpy(E2).pin_memory(), torch.from_numpy(m2).pin_memory(), want_macro=False)
+        assert e.value.status == 1
+    assert g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), want_macro=False) == ok
+    with pytest.raises(gf.GFError):
+        gf.verify(ok | (1 << 63))
 
 
 def test_host_io_pipeline_chunks(gf, torch):
@@ -712,3 +735,39 @@ def test_nuclide_bin_search_sparse_batches(gf, torch, n_iso, grid_type):
         g.set_kernel("auto", nb=flag == "1")
         raw_g, m_g = g.lookup_energies(torch.from_numpy(E).cuda(), torch.from_numpy(mats).cuda(), sort=True)
         assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o), flag
+
+
+@pytest.mark.parametrize("config,hash_", [("C3", 113528), ("C5", 662460)])
+def test_torchrun_two_ranks_strong_split(gf, config, hash_):
+    """The product's N > 1 path end to end: bench.py under torchrun with 2 ranks (gloo, both on this one
+    GPU: GF_DIST_BACKEND), strong split of the config's lookups, one int64
+    all-reduce of the raw sums per step -- the all-reduced hash must be the full batch's golden hash."""
+    import subprocess
+    import sys
+    env = dict(os.environ, GF_DIST_BACKEND="gloo", PYTHONPATH=os.path.dirname(HERE))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(os.path.dirname(HERE), "bench.py"),
+           "--gpus", "2", "--config", config, "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["config"]["lookups_per_rank"] * 2 in (
+        line["config"]["n_lookups"], line["config"]["n_lookups"] + 1)
+    assert line["hash"] == hash_
+
+
+@pytest.mark.parametrize("grid_type", [0, 1, 2])
+def test_ieee_division_path_matches(gf, torch, grid_type):
+    """The FAST = false instantiations of every sorted kernel (tile, group, thread, NB, warp search) and of
+    the unsorted kernel: forced IEEE __ddiv_rn division (the path a grid with a zero-width interval
+    takes; LCG grids never have one) must give the oracle's bits, like the exact reciprocal scheme."""
+    o, g = make_pair(gf, 355 if grid_type else 68, 11303, grid_type)
+    assert g.fastdiv
+    g.set_ieee_division(True)
+    kernels = ["auto", "thread", "warp"] if grid_type == 0 else ["tile", "group", "thread"]
+    for kern in kernels:
+        g.set_kernel(kern)
+        check_lookups(o, g, 1_000_000, 150_000)
+    check_lookups(o, g, 0, 50_000, sort=False)
+    g.set_ieee_division(False)
+    g.set_kernel("auto")

@@ -412,3 +412,18 @@ def test_problem_sizes_closed_form():
     o = O.XSOracle(68, 11303, O.NUCLIDE)
     assert o.npts == 768_604 and o.npts * 48 == 36_892_992
     assert 355 * 11303 == 4_012_565
+
+
+def test_energies_input_domain(xs_small_nuclide):
+    """Caller states must be finite energies with material ids 0..11 (DESIGN.md Sec. 3, caller energies;
+    the same rule as the product, include/gf_xs.h): anything else is rejected before any lookup runs.
+    Finite energies outside [0, 1) are in the domain (the literal algorithm clamps)."""
+    o = xs_small_nuclide
+    E = np.array([0.1, 0.2, 0.3])
+    for bad_e, bad_m in ((np.nan, 0), (np.inf, 1), (-np.inf, 2), (0.5, 12), (0.5, -1)):
+        E2, m2 = E.copy(), np.array([0, 1, 2], dtype=np.int32)
+        E2[1], m2[1] = bad_e, bad_m
+        with pytest.raises(ValueError):
+            o.lookup_energies(E2, m2)
+    raw, m = o.lookup_energies(np.array([-0.5, 0.5, 1.5]), np.array([0, 11, 4], dtype=np.int32))
+    assert 3 <= raw <= 15 and np.isfinite(m).all()

@@ -71,6 +71,10 @@ def main(rnd, *pairs):
         summ[key] = {"kernel": vals.get("Kernel Name", "")[:120], "duration_s": num("gpu__time_duration.sum"),
                      "dram_bytes": (rd or 0) + (wr or 0), "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                     "dram_pct": num("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "lts_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
+                     "l1_hit_pct": num("l1tex__t_sector_hit_rate.pct"),
                      "src": f"profiles/ncu_{rnd}_{key}.txt"}
         print(key, summ[key])
     json.dump(summ, open(summ_path, "w"), indent=1)

@@ -2,8 +2,8 @@
 //   (1) FP64 pipe throughput of non-fused DADD / DMUL (the lookup may not contract to DFMA: R-FP),
 //       and of IEEE __ddiv_rn (the per-micro-evaluation division);
 //   (2) K6: the random 96-B gather bandwidth over a buffer >> L2:
-//       records of 48 B at uniformly random 48-B-aligned offsets, 6 x 16-B loads per gather,
-//       R independent gathers in flight per thread.
+//       96 useful bytes at uniformly random 48-B-aligned (G record pair) or 128-B-aligned (XR
+//       interval record) offsets, R independent gathers in flight per thread, integer XOR folding.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -shared -fmad=false
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -49,27 +49,47 @@ __device__ __forceinline__ uint64_t mix(uint64_t x) {
   return x;
 }
 
-template <int R>
-__global__ void k_gather(const double2 *__restrict__ buf, long long nrec, int per_thread, double *out, uint64_t salt) {
+// K6: R independent random gathers of 96 useful bytes per thread in flight.  Records sit at uniformly
+// random ALIGN-aligned offsets: ALIGN = 48 is the record pair of the nuclide grid G (96 B at a 48-B
+// boundary: 3 or 4 sectors, 6 x 16-B loads), ALIGN = 128 the interval record line of XR (3 x 32-B
+// loads, 3 sectors).  The loaded words are XOR-folded into R independent integer accumulators, so the
+// kernel is bound by the memory system, not by a floating-point dependency chain (round-1 probe).
+// The record index comes from a per-thread 64-bit LCG and a multiply-high.
+template <int R, int ALIGN>
+__global__ void k_gather(const uint64_t *__restrict__ buf, long long nrec, int per_thread,
+                         unsigned long long *out, uint64_t salt) {
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double acc = 0.0;
+  uint64_t s = mix(tid * 0x9e3779b97f4a7c15ull + salt);
+  uint64_t acc[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) acc[r] = 0;
   for (int it = 0; it < per_thread; it += R) {
-    double2 v[R][6];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      // uniform record index in [0, nrec-1) by a multiply-high (no 64-bit modulo on the hot path)
-      long long rec = (long long)__umul64hi(mix(tid * 1315423911ull + (uint64_t)(it + r) * 2654435761ull + salt),
-                                            (uint64_t)(nrec - 1));
-      const double2 *p = buf + rec * 3;  // 48-B record = 3 double2; a pair is 6 double2 (96 B)
+      s = s * 6364136223846793005ull + 1442695040888963407ull;
+      const long long rec = (long long)__umul64hi(s, (uint64_t)(nrec - 1));
+      const uint64_t *p = buf + rec * (ALIGN / 8);
+      if (ALIGN == 128) {
 #pragma unroll
-      for (int k = 0; k < 6; k++) v[r][k] = __ldg(p + k);
+        for (int k = 0; k < 3; k++) {
+          uint64_t a, b, c, d;
+          asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p + 4 * k));
+          acc[r] ^= a ^ b ^ c ^ d;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          uint64_t a, b;
+          asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p + 2 * k));
+          acc[r] ^= a ^ b;
+        }
+      }
     }
-#pragma unroll
-    for (int r = 0; r < R; r++)
-#pragma unroll
-      for (int k = 0; k < 6; k++) acc += v[r][k].x + v[r][k].y;
   }
-  if (acc == 12345.678) out[0] = acc;  // keep the loads alive
+  uint64_t x = 0;
+#pragma unroll
+  for (int r = 0; r < R; r++) x ^= acc[r];
+  if (x == 0x123456789abcdefull) out[0] = x;  // keeps the loads alive
 }
 
 __global__ void k_copy(const double4 *__restrict__ a, double4 *__restrict__ b, long long n) {
@@ -118,30 +138,36 @@ extern "C" double probe_fp64(int which) {
   return ms > 0 ? per_thread * c.blocks * c.threads / (ms * 1e-3) : -1.0;
 }
 
-struct GCtx { const double2 *buf; long long nrec; int blocks, threads, per, R; double *out; uint64_t salt; };
+struct GCtx { const uint64_t *buf; long long nrec; int blocks, threads, per, R, align; unsigned long long *out; uint64_t salt; };
+template <int ALIGN>
+static void launch_ga(GCtx *c) {
+  switch (c->R) {
+    case 1: k_gather<1, ALIGN><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
+    case 2: k_gather<2, ALIGN><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
+    case 4: k_gather<4, ALIGN><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
+    case 8: k_gather<8, ALIGN><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
+    default: k_gather<16, ALIGN><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
+  }
+}
 static void launch_g(void *v) {
   GCtx *c = (GCtx *)v;
   c->salt += 0x9e3779b97f4a7c15ull;
-  switch (c->R) {
-    case 1: k_gather<1><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
-    case 2: k_gather<2><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
-    case 4: k_gather<4><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
-    default: k_gather<8><<<c->blocks, c->threads>>>(c->buf, c->nrec, c->per, c->out, c->salt); break;
-  }
+  if (c->align == 128) launch_ga<128>(c); else launch_ga<48>(c);
 }
 
-// Useful-byte GB/s (96 B per gather) of random record-pair gathers over `bytes` of HBM.
-extern "C" double probe_gather(long long bytes, int R, int threads, int blocks_per_sm) {
+// Useful-byte GB/s (96 B per gather) of random record gathers over `bytes` of HBM (>> L2).
+extern "C" double probe_gather(long long bytes, int R, int threads, int blocks_per_sm, int align) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   GCtx c;
-  c.nrec = bytes / 48;
-  if (cudaMalloc((void **)&c.buf, (size_t)c.nrec * 48) != cudaSuccess) return -1.0;
-  cudaMemset((void *)c.buf, 0, (size_t)c.nrec * 48);
+  c.align = align == 128 ? 128 : 48;
+  c.nrec = bytes / c.align - 2;
+  if (cudaMalloc((void **)&c.buf, (size_t)bytes) != cudaSuccess) return -1.0;
+  cudaMemset((void *)c.buf, 0, (size_t)bytes);
   cudaMalloc(&c.out, 8);
   c.threads = threads;
   c.blocks = sms * blocks_per_sm;
-  c.per = 128;
+  c.per = 256;
   c.R = R;
   c.salt = 1;
   float ms = time_it(launch_g, &c);

@@ -202,9 +202,17 @@ def cpu_baseline(cfg_name, seconds=12.0):
     t = time.perf_counter()
     _, k2 = oracle_run(o, cfg_name, 0, k2, threads)
     dt = time.perf_counter() - t
-    return {"value": k2 / dt, "unit": "lookups/s", "cores": threads, "kind": "oracle",
-            "sample": f"global lookup indices [0, {k2}) of {cfg_name} ({k2 / n:.2%} of the workload), "
-                      f"plain C oracle -O2 -ffp-contract=off, OpenMP {threads} threads, {dt:.1f} s"}
+    res = {"value": k2 / dt, "unit": "lookups/s", "cores": threads, "kind": "oracle",
+           "sample": f"global lookup indices [0, {k2}) of {cfg_name} ({k2 / n:.2%} of the workload), "
+                     f"plain C oracle -O2 -ffp-contract=off, OpenMP {threads} threads, {dt:.1f} s"}
+    if cfg_name in ("C1", "C2"):  # also a 1-thread run for the small configs
+        k1 = max(1000, int(k2 / threads / 4))
+        t = time.perf_counter()
+        _, k1 = oracle_run(o, cfg_name, 0, k1, 1)
+        d1 = time.perf_counter() - t
+        res["single_thread"] = {"value": k1 / d1, "unit": "lookups/s", "cores": 1,
+                                "sample": f"global lookup indices [0, {k1}), 1 thread, {d1:.1f} s"}
+    return res
 
 
 def run_reference(args, rank, world):

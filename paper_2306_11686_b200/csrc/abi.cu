@@ -228,8 +228,11 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
 //   GF_XS_TILE_MIN = smallest batch of the warp-tile kernel in auto mode (default kTileMinN)
 //   GF_XS_GROUP_MIN = smallest batch of the group kernel in auto mode (default kGroupMinN)
 //   GF_XS_NB       = 0: sparse batches search the index grid instead of the NB brackets
-constexpr uint32_t kTileMinN = 6000000u;   // tools/ab_batch_n.py: tile vs group cross at ~4-8 M lookups
-constexpr uint32_t kGroupMinN = 1500000u;  // group vs one lookup per thread cross at ~1-2 M
+// tools/ab_batch_n.py (gpurun_out/r02w): the tile kernel wins from ~2 M lookups (C3 2.125 M: 0.75 ms vs
+// group 0.96, thread 1.17; C4 21.25 M: 4.2 vs 8.1 / 12.0), one lookup per thread below (C3 1 M: 0.68 vs
+// tile 1.02); the group kernel never leads by more than noise (C2 17 M: 1.383 vs 1.387) -- A/B only.
+constexpr uint32_t kTileMinN = 2000000u;
+constexpr uint32_t kGroupMinN = 0xFFFFFFFFu;
 static void kernel_choice(XsDev &X) {
   static_assert(kKernTile == GF_KERN_TILE && kKernWarpSearch == GF_KERN_WARP_SEARCH, "kernel ids");
   X.kern = kKernAuto;

@@ -3,36 +3,42 @@
 //
 // A warp owns a tile of 128 consecutive sorted lookups (lane l: positions 4l .. 4l+3, sorted by energy
 // in registers).  After the locality sort a tile lies in one material and a narrow energy range
-// starting at Emin, so for every nuclide of the material the tile's intervals start at
-// klo = K(Emin), where K(E) = clamp(#{A <= E} - 1, 0, n_gp - 2) is the plain interval
-// (SURVEY.md:520-521).  K is monotone, so for every lookup of the tile (R-TILE)
-//     c(E) = #{m in {1, 2} : A[klo + m] <= E},   K(E) = klo + min(c(E), n_gp - 2 - klo)   if c(E) < 2,
-// and K(E) >= klo + 2 otherwise (then the literal per-lookup search runs; rare for dense batches).
-// The grid-type search therefore runs once per (tile, nuclide) instead of once per (lookup, nuclide),
-// and the two interval records klo, klo + 1 -- one contiguous 256-B piece of the interval-record
-// array XR, whose first doubles are the boundary energies A[klo + 1], A[klo + 2] -- are staged into
-// shared memory by one cp.async.bulk per (tile, nuclide), issued by the lane that found klo.
+// [Emin, Emax], so for every nuclide of the material the tile's intervals form a short run
+// klo .. khi, klo = K(Emin), khi = K(Emax), where K(E) = clamp(#{A <= E} - 1, 0, n_gp - 2) is the
+// plain interval (SURVEY.md:520-521).  K is monotone, so for every lookup of the tile (R-TILE,
+// DESIGN.md Sec. 3)
+//     K(E) = klo + #{m in 0 .. khi - klo - 1 : A[klo + 1 + m] <= E},
+// and the boundaries A[klo + 1 + m] are the first doubles of the interval records klo + m of XR.  The
+// grid-type search therefore runs twice per (tile, nuclide) instead of once per (lookup, nuclide), and
+// the run's records klo .. khi -- one contiguous piece of XR -- are staged into shared memory by one
+// cp.async.bulk per (tile, nuclide), issued by the lane that searched it.
 //
-// Pipeline per warp (no producer warp, no CTA barrier): the nuclides of the material are walked in
-// chunks of 16; chunk c's records are copied into one of two SMEM buffers while chunk c-1 is
-// computed, and the grid-type search of chunk c+2 is issued before chunk c is computed, so neither
-// the index-grid load nor the bulk copy is on the critical path after a tile's first two chunks.
-// The nuclide loop reads only shared memory: the slot's {record index, clamp}, the two boundaries and
-// one record (LDS broadcasts: the lanes of a warp nearly always share the slot's record).
+// Runs are variable-length and packed: a chunk takes as many of the material's nuclides (<= 32, one
+// per lane) as fit kCap records (a warp scan of the run lengths), so dense batches (17 M lookups: runs
+// of ~1.6 records) stage ~25 nuclides per chunk and sparse ones (2 M lookups, one GPU's share of an
+// 8-way split: ~6 records) fewer -- the kernel has no density threshold.  Pipeline per warp (no
+// producer warp, no CTA barrier): two SMEM buffers; chunk c+1 is in flight while chunk c is computed,
+// and the searches of the chunk after that are issued before chunk c is computed.  The nuclide loop
+// reads only shared memory: the slot's {record index, offset, length}, the boundaries (a count over
+// <= 1 boundary in the common case, a binary search in general) and one record (LDS broadcasts).
 //
-// Grid types: unionized (klo from the index grid at the tile's smallest union index), hash (the
-// literal hash search at Emin; the tile takes this path only if every lookup lies strictly inside
-// its hash bin, RN(b du) < E < RN((b+1) du), where the literal edge rules cannot fire and the
-// literal search returns K(E) -- DESIGN.md R-TILE), and kGridNB (per-nuclide bin brackets, no index
-// grid).  Tiles that straddle a material boundary or the batch end, or hold energies outside
-// [+0, 2] (caller energies), take the one-by-one path with the literal per-lookup search.
+// Grid types: unionized (klo / khi from the index grid at the tile's extreme union indices), hash (the
+// literal hash search; the tile takes this path only if every lookup lies strictly inside its hash
+// bin, RN(b du) < E < RN((b+1) du), where the literal edge rules cannot fire and the literal search
+// returns K(E) -- DESIGN.md R-TILE), and kGridNB (per-nuclide bin brackets, no index grid).  Tiles
+// that straddle a material boundary or the batch end, or hold energies outside [+0, 2] (caller
+// energies), take the one-by-one path with the literal per-lookup search.
 #pragma once
 
+#ifndef GF_ODD_FIRST
+#define GF_ODD_FIRST 1  // hand out the tiles across material boundaries first
+#endif
 constexpr int kTileTpb = 128;  // 4 warps per CTA
 constexpr int kTileWarps = kTileTpb / 32;
-constexpr int kChunk = 10;     // nuclides per staged chunk (lanes 0..9 stage one each; 4 CTAs fit an SM)
-constexpr int kRecs = 4;       // interval records staged per (tile, nuclide): klo .. klo + 3
-constexpr int kSlotBytes = 128 * kRecs;
+#ifndef GF_TILE_CAP
+#define GF_TILE_CAP 40
+#endif
+constexpr int kCap = GF_TILE_CAP;  // records per staging buffer (5.6 KB; two per warp, 4 CTAs of 4 warps fit an SM)
 
 // mbarrier / bulk-copy (TMA 1-D) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -60,42 +66,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                : "memory");
 }
 
+// Records sit at a 144-B stride in shared memory (128 B + 16 B of padding): the lanes of a warp read the
+// same field of up to 8 neighbouring records without bank conflicts (at a 128-B stride they would all
+// map to the same banks; ncu: 53% of the LDS wavefronts were conflicts at 2 M lookups).
+constexpr int kRecStride = 144;
+
 struct TileSmem {  // per warp
-  unsigned char rec[2][kChunk][kSlotBytes];  // [buffer][slot]: records klo .. klo + kRecs - 1
-  uint2 meta[2][kChunk];                     // {record index of klo, n_gp - 2 - klo}
-  uint64_t bar[2];                           // one mbarrier per buffer (transaction count = staged bytes)
+  unsigned char rec[2][kCap][kRecStride];  // [buffer]: the chunk's runs of interval records, packed
+  uint2 meta[2][32];                // [buffer][slot]: {record index of klo, offset | length << 8 | wide << 16}
+  uint64_t bar[2];                  // one mbarrier per buffer (transaction count = staged bytes)
 };
 
 __host__ __device__ inline size_t tile_table_bytes(int total) { return (xs_table_smem(total) + 127) & ~size_t(127); }
 __host__ __device__ inline size_t tile_smem(int total) {
   return tile_table_bytes(total) + sizeof(TileSmem) * kTileWarps;
-}
-
-// klo of the nuclide of entry e for the tile (one lane): the grid type's literal search at Emin.
-template <int GT>
-__device__ __forceinline__ uint32_t tile_klo(const XsDev &X, uint2 e, double Emin, uint32_t imin) {
-  if (GT == GF_GRID_UNIONIZED) return __ldg(X.IG + e.y + imin);  // (the index grid is clamped to n_gp - 2)
-  long long ia = imin;
-  if (GT == kGridNB) ia = energy_index<kGridNB>(X, Emin);
-  return interval<GT>(X, e, Emin, ia);
-}
-
-// Stages chunk [c0, c0 + 16) of the material's entries into buffer b: lane l < 16 copies records
-// klo, klo + 1 of entry c0 + l.  klo: this lane's tile_klo for that entry.
-__device__ __forceinline__ void tile_stage(const XsDev &X, const XsTables &T, TileSmem &S, int b, int c0, int j1,
-                                           uint32_t klo) {
-  const int lane = threadIdx.x & 31;
-  const int cnt = min(kChunk, j1 - c0);
-  if (lane == 0) mbar_arrive_tx(&S.bar[b], (uint32_t)(cnt * kSlotBytes));
-  __syncwarp();
-  if (lane < cnt) {
-    const uint2 e = tab_ent(T, c0 + lane, true);
-    const uint32_t kb = e.x + klo;
-    const uint32_t nucbase = (e.x / (uint32_t)X.n_gp) * (uint32_t)X.n_gp;  // e.x = nuc n_gp (+ k0 < n_gp)
-    S.meta[b][lane] = make_uint2(kb, (uint32_t)(X.n_gp - 2) - (kb - nucbase));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's previous generic reads
-    bulk_g2s(S.rec[b][lane], X.XR + (size_t)kb * 16, kSlotBytes, &S.bar[b]);
-  }
 }
 
 // One interval record from shared memory (its v0.x = E[k+1], ..., y at double 12).  Plain loads through
@@ -110,20 +94,6 @@ __device__ __forceinline__ void load_rec_smem(const unsigned char *a, Rec &R) {
   R.v4 = q[4];
   R.v5 = q[5];
   if (FAST) R.y = reinterpret_cast<const double *>(a)[12];
-}
-
-// (unused) The same with volatile LDS: for conditional reloads, which the compiler must not hoist (hoisted
-// speculative copies of the record would need another 26 registers per reload).
-template <bool FAST>
-__device__ __forceinline__ void load_rec_smem_v(const unsigned char *a, Rec &R) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(a);
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(R.v0.x), "=d"(R.v0.y) : "r"(s) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2 + 16];" : "=d"(R.v1.x), "=d"(R.v1.y) : "r"(s) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2 + 32];" : "=d"(R.v2.x), "=d"(R.v2.y) : "r"(s) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2 + 48];" : "=d"(R.v3.x), "=d"(R.v3.y) : "r"(s) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2 + 64];" : "=d"(R.v4.x), "=d"(R.v4.y) : "r"(s) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2 + 80];" : "=d"(R.v5.x), "=d"(R.v5.y) : "r"(s) : "memory");
-  if (FAST) asm volatile("ld.shared.f64 %0, [%1 + 96];" : "=d"(R.y) : "r"(s) : "memory");
 }
 
 // Predicated reload (one asm statement, no branch): lanes with p reload R from shared address a, the
@@ -141,94 +111,151 @@ __device__ __forceinline__ void reload_rec_smem_if(uint32_t a, bool p, Rec &R) {
       : "memory");
 }
 
-// c(E) = #{m < min(kRecs, lim) : A[klo + 1 + m] <= E}: the interval of E relative to klo when
-// c < kRecs (R-TILE; m < lim masks the slot's records beyond the nuclide's last interval).  Bit
-// patterns of non-negative doubles order as signed 64-bit integers.
-__device__ __forceinline__ uint32_t slot_count(long long eb, const long long (&bb)[kRecs], const bool (&pm)[kRecs]) {
-  uint32_t c = 0;
-#pragma unroll
-  for (int m = 0; m < kRecs; m++) c += (pm[m] && eb >= bb[m]) ? 1u : 0u;
-  return c;
+__device__ __forceinline__ long long smem_bits(const unsigned char *a) { return *reinterpret_cast<const long long *>(a); }
+
+// The grid type's literal search for the tile at energy E with grid index ix (union index / hash bin;
+// kGridNB bins the energy itself).
+template <int GT>
+__device__ __forceinline__ uint32_t tile_k(const XsDev &X, uint2 e, double E, uint32_t ix) {
+  if (GT == GF_GRID_UNIONIZED) return __ldg(X.IG + e.y + ix);  // (the index grid is clamped to n_gp - 2)
+  long long ia = ix;
+  if (GT == kGridNB) ia = energy_index<kGridNB>(X, E);
+  return interval<GT>(X, e, E, ia);
 }
 
-__device__ __forceinline__ long long smem_bits(const unsigned char *a) { return *reinterpret_cast<const long long *>(a); }
+// The runs of the next candidate nuclides (lane l: entry c0 + l): klo = K(Emin), khi = K(Emax).
+struct RunSearch {
+  uint32_t klo, khi;
+};
+template <int GT>
+__device__ __forceinline__ RunSearch tile_search(const XsDev &X, const XsTables &T, int c0, int j1, double Emin,
+                                                 double Emax, uint32_t imin, uint32_t imax) {
+  const int j = c0 + (int)(threadIdx.x & 31);
+  RunSearch r{0u, 0u};
+  if (j < j1) {
+    const uint2 e = tab_ent(T, j, true);
+    r.klo = tile_k<GT>(X, e, Emin, imin);
+    r.khi = tile_k<GT>(X, e, Emax, imax);
+  }
+  return r;
+}
+
+// Stages the runs of entries c0, c0 + 1, ... into buffer b: as many as fit kCap records (a prefix of the
+// 32 candidates, at least one: a run longer than kCap is cut to kCap records and marked wide).  Returns
+// the number of entries staged.  All 32 lanes call it.
+__device__ __forceinline__ int tile_stage(const XsDev &X, const XsTables &T, TileSmem &S, int b, int c0, int j1,
+                                          RunSearch r) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = c0 + lane < j1;
+  uint32_t cnt = valid ? r.khi - r.klo + 1u : 0u;
+  const uint32_t wide = cnt > (uint32_t)kCap ? 1u : 0u;
+  cnt = min(cnt, (uint32_t)kCap);
+  uint32_t incl = cnt;  // inclusive warp scan of the run lengths
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const bool fits = valid && incl <= (uint32_t)kCap;  // a prefix of the lanes (every valid run has >= 1 record)
+  const int nsel = __popc(__ballot_sync(0xffffffffu, fits));
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, nsel > 0 ? nsel - 1 : 0);
+  if (lane == 0) mbar_arrive_tx(&S.bar[b], total * 128u);
+  __syncwarp();
+  if (fits) {
+    const uint2 e = tab_ent(T, c0 + lane, true);
+    const uint32_t kb = e.x + r.klo, off = incl - cnt;
+    S.meta[b][lane] = make_uint2(kb, off | (cnt << 8) | (wide << 16));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's previous generic reads
+    for (uint32_t k = 0; k < cnt; k++)  // one bulk copy per record (the SMEM stride is padded)
+      bulk_g2s(S.rec[b][off + k], X.XR + (size_t)(kb + k) * 16, 128u, &S.bar[b]);
+  }
+  return nsel;
+}
+
+// #{m < nbd : boundary m <= E}, the boundaries being the first doubles of the records at `rec` (kRecStride
+// stride, sorted): a branch-free binary search whose steps depend on nbd only (warp-uniform).  Bit
+// patterns of non-negative doubles order as signed 64-bit integers.
+__device__ __forceinline__ uint32_t run_count(const unsigned char *rec, uint32_t nbd, long long eb) {
+  uint32_t c = 0;
+  if (nbd == 0) return 0;
+  for (uint32_t step = 1u << (31 - __clz(nbd)); step; step >>= 1)
+    if (c + step <= nbd && eb >= smem_bits(rec + kRecStride * (c + step - 1))) c += step;
+  return c;
+}
 
 template <int GT, bool FAST>
 __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, TileSmem &S, uint32_t (&phase),
                                           const double (&E)[kL], const uint32_t (&ix)[kL], int j0, int j1,
-                                          double Emin, uint32_t imin, double (&m)[kL][5]) {
-  const int lane = threadIdx.x & 31;
+                                          double Emin, double Emax, uint32_t imin, uint32_t imax,
+                                          double (&m)[kL][5]) {
   long long eb[kL];
 #pragma unroll
   for (int i = 0; i < kL; i++) eb[i] = __double_as_longlong(E[i]);
   __syncwarp();  // the previous tile's readers of S are done
-  // prologue: stage chunks 0 and 1
+  // prologue: stage chunks 0 and 1, search the candidates after them
+  int cs0 = j0, cn0, cs1, cn1 = 0, nxt;
   {
-    const bool a = lane < kChunk && j0 + lane < j1, b = lane < kChunk && j0 + kChunk + lane < j1;
-    const uint2 ea = tab_ent(T, a ? j0 + lane : j0, true), ebn = tab_ent(T, b ? j0 + kChunk + lane : j0, true);
-    const uint32_t ka = a ? tile_klo<GT>(X, ea, Emin, imin) : 0u;
-    const uint32_t kbn = b ? tile_klo<GT>(X, ebn, Emin, imin) : 0u;
-    tile_stage(X, T, S, 0, j0, j1, ka);
-    if (j0 + kChunk < j1) tile_stage(X, T, S, 1, j0 + kChunk, j1, kbn);
+    RunSearch r = tile_search<GT>(X, T, j0, j1, Emin, Emax, imin, imax);
+    cn0 = tile_stage(X, T, S, 0, j0, j1, r);
+    cs1 = j0 + cn0;
+    if (cs1 < j1) {
+      r = tile_search<GT>(X, T, cs1, j1, Emin, Emax, imin, imax);
+      cn1 = tile_stage(X, T, S, 1, cs1, j1, r);
+    }
+    nxt = cs1 + cn1;
   }
+  RunSearch pend = tile_search<GT>(X, T, nxt, j1, Emin, Emax, imin, imax);
   int b = 0;
-  for (int c0 = j0; c0 < j1; c0 += kChunk, b ^= 1) {
-    // grid-type search of chunk c + 2 (consumed when this chunk is done)
-    const int c2 = c0 + 2 * kChunk;
-    const bool s2 = lane < kChunk && c2 + lane < j1;
-    const uint32_t k2 = s2 ? tile_klo<GT>(X, tab_ent(T, c2 + lane, true), Emin, imin) : 0u;
+  while (cs0 < j1) {
     mbar_wait(&S.bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;
     __syncwarp();
-    const int ce = min(c0 + kChunk, j1);
 #pragma unroll 1
-    for (int jj = c0; jj < ce; jj++) {
-      const int s = jj - c0;
+    for (int s = 0; s < cn0; s++) {
+      const int jj = cs0 + s;
       const uint2 mt = S.meta[b][s];
-      const uint32_t kb = mt.x, lim = mt.y;
-      const unsigned char *ra = S.rec[b][s];
-      // boundaries A[klo + 1 + m] = the staged records' first doubles
-      long long bb[kRecs];
-      bool pm[kRecs];
-#pragma unroll
-      for (int q = 0; q < kRecs; q++) {
-        bb[q] = smem_bits(ra + 128 * q);
-        pm[q] = (uint32_t)q < lim;
-      }
-      const uint32_t ca = slot_count(eb[0], bb, pm), cd = slot_count(eb[kL - 1], bb, pm);
+      const uint32_t off = mt.y & 0xFFu, cnt = (mt.y >> 8) & 0xFFu;
+      const bool wide = (mt.y >> 16) != 0u;
+      const unsigned char *ra = S.rec[b][off];
+      const uint32_t nbd = cnt - 1u;  // staged boundaries A[klo + 1 .. klo + cnt - 1]
+      // lookup 0 by a binary search over the run; the thread's other lookups (a much narrower range)
+      // against the next three boundaries: c_i = ca + [E_i >= bx] + [E_i >= by] while E_i < bz
+      const uint32_t ca = run_count(ra, nbd, eb[0]);
+      const long long kInf = 0x7FF0000000000000ll;  // (+inf: no boundary)
+      const long long bx = ca < nbd ? smem_bits(ra + kRecStride * ca) : kInf;
+      const long long by = ca + 1u < nbd ? smem_bits(ra + kRecStride * (ca + 1u)) : kInf;
+      const long long bz = ca + 2u < nbd ? smem_bits(ra + kRecStride * (ca + 2u)) : kInf;
+      const uint32_t cd = ca + (eb[kL - 1] >= bx ? 1u : 0u) + (eb[kL - 1] >= by ? 1u : 0u);
       const double conc = tab_conc(T, jj, true);
       Rec P;
-      // common case: every lookup of the warp lies in a staged record and no thread's lookups span two
-      // boundaries; then lookup i > 0 is in record ca + [E_i >= A[klo + 1 + ca]]
-      if (!__any_sync(0xffffffffu, cd >= (uint32_t)kRecs || cd > ca + 1u)) {
+      // common case: no lookup of the warp beyond a cut run, and no thread's lookups span more than two
+      // boundaries (E_3 < bz)
+      if (!__any_sync(0xffffffffu, (wide && cd == nbd) || eb[kL - 1] >= bz)) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(ra);
-        long long bx = bb[0];
-#pragma unroll
-        for (int q = 1; q < kRecs; q++) bx = ca == (uint32_t)q ? bb[q] : bx;
         uint32_t cP = ca;
-        load_rec_smem<FAST>(ra + 128 * ca, P);
+        load_rec_smem<FAST>(ra + kRecStride * ca, P);
         if (!__any_sync(0xffffffffu, ca != cd)) {  // no thread straddles: the 4 chains interleave
 #pragma unroll
           for (int i = 0; i < kL; i++) accumulate_rec<FAST>(P, E[i], conc, m[i]);
         } else {
-        accumulate_rec<FAST>(P, E[0], conc, m[0]);
+          accumulate_rec<FAST>(P, E[0], conc, m[0]);
 #pragma unroll
-        for (int i = 1; i < kL; i++) {
-          // lanes whose lookup i is past their boundary reload (predicated LDS; ptxas spills if this is
-          // a branch around plain loads)
-          const uint32_t c = (i == kL - 1) ? cd : ca + (eb[i] >= bx && ca != cd ? 1u : 0u);
-          reload_rec_smem_if(sa + 128 * c, c != cP, P);
-          cP = c;
-          accumulate_rec<FAST>(P, E[i], conc, m[i]);
+          for (int i = 1; i < kL; i++) {
+            // lanes whose lookup i is past their boundary reload (predicated LDS; ptxas spills if this
+            // is a branch around plain loads)
+            const uint32_t c = (i == kL - 1) ? cd : ca + (eb[i] >= bx ? 1u : 0u) + (eb[i] >= by ? 1u : 0u);
+            reload_rec_smem_if(sa + kRecStride * c, c != cP, P);
+            cP = c;
+            accumulate_rec<FAST>(P, E[i], conc, m[i]);
+          }
         }
-        }
-      } else {  // some thread spans two boundaries or has K(E) >= klo + kRecs: per lookup (rare)
+      } else {  // three boundaries inside some thread's lookups, or a lookup beyond a cut run: per lookup
 #pragma unroll
         for (int i = 0; i < kL; i++) {
-          const uint32_t c = slot_count(eb[i], bb, pm);
-          if (c < (uint32_t)kRecs) {
-            load_rec_smem<FAST>(ra + 128 * c, P);
-          } else {  // the literal search
+          const uint32_t c = run_count(ra, nbd, eb[i]);
+          if (!(wide && c == nbd)) {
+            load_rec_smem<FAST>(ra + kRecStride * c, P);
+          } else {  // beyond the staged part of a cut run: the literal search
             const uint2 e = tab_ent(T, jj, true);
             long long id = ix[i];
             if (GT == kGridNB) id = energy_index<kGridNB>(X, E[i]);
@@ -239,7 +266,17 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
       }
     }
     __syncwarp();  // every lane is done with buffer b
-    if (c2 < j1) tile_stage(X, T, S, b, c2, j1, k2);
+    int cn2 = 0;
+    if (nxt < j1) {
+      cn2 = tile_stage(X, T, S, b, nxt, j1, pend);
+      pend = tile_search<GT>(X, T, nxt + cn2, j1, Emin, Emax, imin, imax);
+    }
+    cs0 = cs1;
+    cn0 = cn1;
+    cs1 = nxt;
+    cn1 = cn2;
+    nxt += cn2;
+    b ^= 1;
   }
 }
 
@@ -279,6 +316,21 @@ __device__ __forceinline__ void lookups_one_by_one(const XsDev &X, const XsTable
   }
 }
 
+__device__ __forceinline__ bool ok_energies(const double (&E)[kL]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < kL; i++) ok = ok && __double_as_longlong(E[i]) >= 0 && E[i] <= 2.0;
+  return ok;
+}
+
+__device__ __forceinline__ long long warp_max64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
 __device__ __forceinline__ long long warp_min64(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -291,6 +343,51 @@ __device__ __forceinline__ long long warp_min64(long long v) {
 #ifndef GF_TILE_MINB
 #define GF_TILE_MINB 4
 #endif
+
+// One lane of a tile with odd energies (caller states outside [+0, 2], hash lookups on a bin edge): the
+// group kernel's pipelined loop if its 4 lookups share a material, else one by one.
+template <int GT, bool FAST>
+__device__ __forceinline__ void odd_lane(const XsDev &X, const XsTables &T, const uint32_t *ms, uint32_t p0,
+                                      uint32_t nl, double (&E)[kL], uint32_t (&ix)[kL], double (&m)[kL][5],
+                                      uint32_t &perm) {
+  int lm0 = 0, lm1 = 0;
+#pragma unroll
+  for (int mm = 1; mm < kMats; mm++) {
+    if (p0 >= ms[mm]) lm0 = mm;
+    if (p0 + nl - 1 >= ms[mm]) lm1 = mm;
+  }
+  const bool fast = FAST && GT != kGridNB && nl == kL && ok_energies(E);
+  if (fast && lm0 == lm1) {
+    local_sort(E, ix, perm);
+    const int j0 = T.off[lm0], j1 = T.off[lm0 + 1];
+    if (j1 > j0) group_loop<GT, FAST>(X, T, E, ix, j0, j1, m);
+  } else {
+    lookups_one_by_one<GT, FAST>(X, T, ms, p0, nl, E, ix, m);
+  }
+}
+
+// The 4 sorted lookups of lane position p0 (nl of them; missing ones repeat the last, or E = 0 if none).
+template <int GT>
+__device__ __forceinline__ void load_tile_lookups(const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
+                                                  uint32_t p0, uint32_t nl, double (&E)[kL], uint32_t (&ix)[kL]) {
+  if (nl == kL) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(E[0]), "=d"(E[1]), "=d"(E[2]), "=d"(E[3]) : "l"(Es + p0));
+    if (GT != kGridNB) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(ixs + p0));
+      ix[0] = v.x; ix[1] = v.y; ix[2] = v.z; ix[3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kL; i++) ix[i] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kL; i++) {
+      const uint32_t p = nl ? p0 + min((uint32_t)i, nl - 1) : 0u;
+      E[i] = nl ? Es[p] : 0.0;
+      ix[i] = (nl && GT != kGridNB) ? ixs[p] : 0u;
+    }
+  }
+}
 
 // ix: the per-lookup grid index from idx_prep (union index / hash bin); unused for kGridNB.
 template <int GT, bool FAST>
@@ -315,40 +412,52 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
   const uint32_t ntiles = (n + 32 * kL - 1) / (32 * kL);
   double du = 0.0;
   if (GT == GF_GRID_HASH) du = __ddiv_rn(1.0, (double)X.bins);
-  // dynamic tile scheduling: a warp takes the next tile when it finishes one (tiles of the 321-nuclide
-  // fuel come first in the sorted order, so the heavy tiles are handed out first)
-  for (uint32_t t = next_tile(work); t < ntiles; t = next_tile(work)) {
+  // dynamic tile scheduling: a warp takes the next work item when it finishes one.  The tiles across a
+  // material boundary or at the batch end (<= 13: one pass per material, the longest tiles) are handed
+  // out first, then the rest in sorted order (the 321-nuclide fuel first), so long tiles start early.
+  __shared__ uint32_t s_odd[kMats + 1];
+  __shared__ int s_nodd;
+  if (threadIdx.x == 0) {
+    int no = 0;
+    for (int mm = 1; mm <= kMats; mm++) {
+      const uint32_t b = mm < kMats ? ms[mm] : n;  // (ms is non-decreasing: the list comes out sorted)
+      const uint32_t tb = b / (32 * kL);
+      if (b % (32 * kL) != 0u && tb < ntiles && (no == 0 || s_odd[no - 1] != tb)) s_odd[no++] = tb;
+    }
+    s_nodd = no;
+  }
+  __syncthreads();
+  const int nodd = GF_ODD_FIRST ? s_nodd : 0;
+  for (uint32_t w = next_tile(work); w < ntiles; w = next_tile(work)) {
+    uint32_t t;
+    if (w < (uint32_t)nodd) {
+      t = s_odd[w];
+    } else {  // the (w - nodd)-th tile not in the list
+      t = w - (uint32_t)nodd;
+      for (int q = 0; q < nodd; q++)
+        if (s_odd[q] <= t) t++;
+    }
     const uint32_t P = t * 32 * kL;
     const uint32_t p0 = P + lane * kL;
     const uint32_t nl = p0 < n ? min((uint32_t)kL, n - p0) : 0u;
+    const uint32_t plast = min(P + 32 * kL, n) - 1;
+    int mat0 = 0, mat1 = 0;
+#pragma unroll
+    for (int mm = 1; mm < kMats; mm++) {
+      if (P >= ms[mm]) mat0 = mm;
+      if (plast >= ms[mm]) mat1 = mm;
+    }
+    // tile path: energies in [+0, 2] (hash grid: strictly inside the bin).  A tile across a material
+    // boundary (or the batch end) runs one pass per material: the pass's lookups are the active ones,
+    // the others (and missing ones) take a copy of an active energy of their lane -- computed and
+    // discarded -- so every pass is an ordinary tile over one material's nuclides.
     double E[kL];
     uint32_t ix[kL];
-    double m[kL][5];
-    if (nl == kL) {
-      asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(E[0]), "=d"(E[1]), "=d"(E[2]), "=d"(E[3]) : "l"(Es + p0));
-      if (GT != kGridNB) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(ixs + p0));
-        ix[0] = v.x; ix[1] = v.y; ix[2] = v.z; ix[3] = v.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < kL; i++) ix[i] = 0;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < kL; i++) {
-        const uint32_t p = nl ? p0 + min((uint32_t)i, nl - 1) : 0u;
-        E[i] = nl ? Es[p] : 0.0;
-        ix[i] = (nl && GT != kGridNB) ? ixs[p] : 0u;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kL; i++)
-#pragma unroll
-      for (int c = 0; c < 5; c++) m[i][c] = 0.0;
-    // tile path: whole tile in one material, energies in [+0, 2] (hash grid: strictly inside the bin)
-    bool ok = FAST && nl == kL;
+    bool ok = FAST;
+    load_tile_lookups<GT>(Es, ixs, p0, nl, E, ix);
 #pragma unroll
     for (int i = 0; i < kL; i++) {
+      if ((uint32_t)i >= nl) continue;
       const long long bits = __double_as_longlong(E[i]);
       ok = ok && bits >= 0 && E[i] <= 2.0;
       if (GT == GF_GRID_HASH) {
@@ -357,29 +466,61 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
         ok = ok && lo < E[i] && E[i] < hi;
       }
     }
-    const uint32_t plast = min(P + 32 * kL, n) - 1;
-    int mat0 = 0, mat1 = 0;
+    if (__all_sync(0xffffffffu, ok)) {
+      for (int mt = mat0; mt <= mat1; mt++) {
+        uint32_t act = 0;  // bit i: lookup i of this lane is in the pass (material segment [ms[mt], ms[mt+1]))
+        const uint32_t sb = ms[mt], se = mt + 1 < kMats ? ms[mt + 1] : n;
 #pragma unroll
-    for (int mm = 1; mm < kMats; mm++) {
-      if (P >= ms[mm]) mat0 = mm;
-      if (plast >= ms[mm]) mat1 = mm;
-    }
-    const bool tile = __all_sync(0xffffffffu, ok) && mat0 == mat1;
-    uint32_t perm = 0x76543210u;
-    if (tile) {
-      local_sort(E, ix, perm);
-      const double Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
-      const uint32_t imin = __reduce_min_sync(0xffffffffu, ix[0]);
-      const int j0 = T.off[mat0], j1 = T.off[mat0 + 1];
-      if (j1 > j0) tile_loop<GT, FAST>(X, T, S, phase, E, ix, j0, j1, Emin, imin, m);
-    } else if (nl) {
-      lookups_one_by_one<GT, FAST>(X, T, ms, p0, nl, E, ix, m);
-    }
+        for (int i = 0; i < kL; i++) act |= ((uint32_t)i < nl && p0 + i >= sb && p0 + i < se) ? (1u << i) : 0u;
+        if (!__any_sync(0xffffffffu, act != 0u)) continue;
+        if (mt != mat0) load_tile_lookups<GT>(Es, ixs, p0, nl, E, ix);  // (not kept live across passes)
+        // stand-in for inactive lookups: the lane's first active lookup, else the warp's smallest active energy
+        long long a0 = 0x7FF0000000000000ll;
+        uint32_t x0 = 0;
 #pragma unroll
-    for (uint32_t i = 0; i < (uint32_t)kL; i++) {
-      if (i < nl) {
-        vacc += argmax5_plus1(m[i]);
-        if (out.any()) write_out<5>(out, idx[p0 + ((perm >> (4 * i)) & 15u)], m[i]);
+        for (int i = kL - 1; i >= 0; i--)
+          if (act & (1u << i)) { a0 = __double_as_longlong(E[i]); x0 = ix[i]; }
+        const long long wmin = warp_min64(a0);
+        const uint32_t wx = __shfl_sync(0xffffffffu, x0, __ffs(__ballot_sync(0xffffffffu, a0 == wmin)) - 1);
+        if (act == 0u) { a0 = wmin; x0 = wx; }
+#pragma unroll
+        for (int i = 0; i < kL; i++)
+          if (!(act & (1u << i))) { E[i] = __longlong_as_double(a0); ix[i] = x0; }
+        uint32_t perm = 0x76543210u;
+        local_sort(E, ix, perm);
+        double m[kL][5];
+#pragma unroll
+        for (int i = 0; i < kL; i++)
+#pragma unroll
+          for (int c = 0; c < 5; c++) m[i][c] = 0.0;
+        const double Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
+        const double Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
+        const uint32_t imin = __reduce_min_sync(0xffffffffu, ix[0]), imax = __reduce_max_sync(0xffffffffu, ix[kL - 1]);
+        const int j0 = T.off[mt], j1 = T.off[mt + 1];
+        if (j1 > j0) tile_loop<GT, FAST>(X, T, S, phase, E, ix, j0, j1, Emin, Emax, imin, imax, m);
+#pragma unroll
+        for (int i = 0; i < kL; i++) {  // slot i holds lookup q; the pass finishes its active lookups
+          const uint32_t q = (perm >> (4 * i)) & 15u;
+          if (act & (1u << q)) {
+            vacc += argmax5_plus1(m[i]);
+            if (out.any()) write_out<5>(out, idx[p0 + q], m[i]);
+          }
+        }
+      }
+    } else if (nl) {  // odd energies (caller states): each lane on its own
+      double m[kL][5];
+#pragma unroll
+      for (int i = 0; i < kL; i++)
+#pragma unroll
+        for (int c = 0; c < 5; c++) m[i][c] = 0.0;
+      uint32_t perm = 0x76543210u;
+      odd_lane<GT, FAST>(X, T, ms, p0, nl, E, ix, m, perm);
+#pragma unroll
+      for (uint32_t i = 0; i < (uint32_t)kL; i++) {
+        if (i < nl) {
+          vacc += argmax5_plus1(m[i]);
+          if (out.any()) write_out<5>(out, idx[p0 + ((perm >> (4 * i)) & 15u)], m[i]);
+        }
       }
     }
   }

@@ -10,14 +10,14 @@
 //     K(E) = klo + #{m in 0 .. khi - klo - 1 : A[klo + 1 + m] <= E},
 // and the boundaries A[klo + 1 + m] are the first doubles of the interval records klo + m of XR.  The
 // grid-type search therefore runs twice per (tile, nuclide) instead of once per (lookup, nuclide), and
-// the run's records klo .. khi -- one contiguous piece of XR -- are staged into shared memory by one
-// cp.async.bulk per (tile, nuclide), issued by the lane that searched it.
+// the run's records klo .. khi -- one contiguous piece of XR -- are staged into shared memory by the
+// warp (16-B cp.async pieces, the chunk's records spread over the lanes).
 //
 // Runs are variable-length and packed: a chunk takes as many of the material's nuclides (<= 32, one
 // per lane) as fit kCap records (a warp scan of the run lengths), so dense batches (17 M lookups: runs
 // of ~1.6 records) stage ~25 nuclides per chunk and sparse ones (2 M lookups, one GPU's share of an
 // 8-way split: ~6 records) fewer -- the kernel has no density threshold.  Pipeline per warp (no
-// producer warp, no CTA barrier): two SMEM buffers; chunk c+1 is in flight while chunk c is computed,
+// producer warp, no CTA barrier; cp.async groups): two SMEM buffers; chunk c+1 is in flight while chunk c is computed,
 // and the searches of the chunk after that are issued before chunk c is computed.  The nuclide loop
 // reads only shared memory: the slot's {record index, offset, length}, the boundaries (a count over
 // <= 1 boundary in the common case, a binary search in general) and one record (LDS broadcasts).
@@ -40,31 +40,7 @@ constexpr int kTileWarps = kTileTpb / 32;
 #endif
 constexpr int kCap = GF_TILE_CAP;  // records per staging buffer (5.6 KB; two per warp, 4 CTAs of 4 warps fit an SM)
 
-// mbarrier / bulk-copy (TMA 1-D) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 // Records sit at a 144-B stride in shared memory (128 B + 16 B of padding): the lanes of a warp read the
 // same field of up to 8 neighbouring records without bank conflicts (at a 128-B stride they would all
@@ -74,7 +50,7 @@ constexpr int kRecStride = 144;
 struct TileSmem {  // per warp
   unsigned char rec[2][kCap][kRecStride];  // [buffer]: the chunk's runs of interval records, packed
   uint2 meta[2][32];                // [buffer][slot]: {record index of klo, offset | length << 8 | wide << 16}
-  uint64_t bar[2];                  // one mbarrier per buffer (transaction count = staged bytes)
+  uint32_t src[kCap];               // record index (in XR) of each staged record of the chunk being staged
 };
 
 __host__ __device__ inline size_t tile_table_bytes(int total) { return (xs_table_smem(total) + 127) & ~size_t(127); }
@@ -83,7 +59,7 @@ __host__ __device__ inline size_t tile_smem(int total) {
 }
 
 // One interval record from shared memory (its v0.x = E[k+1], ..., y at double 12).  Plain loads through
-// a pointer into the extern __shared__ array: they compile to LDS and stay after the mbarrier wait.
+// a pointer into the extern __shared__ array: they compile to LDS and stay after the cp.async wait.
 template <bool FAST>
 __device__ __forceinline__ void load_rec_smem(const unsigned char *a, Rec &R) {
   const double2 *q = reinterpret_cast<const double2 *>(a);
@@ -142,7 +118,8 @@ __device__ __forceinline__ RunSearch tile_search(const XsDev &X, const XsTables 
 
 // Stages the runs of entries c0, c0 + 1, ... into buffer b: as many as fit kCap records (a prefix of the
 // 32 candidates, at least one: a run longer than kCap is cut to kCap records and marked wide).  Returns
-// the number of entries staged.  All 32 lanes call it.
+// the number of entries staged.  All 32 lanes call it; every lane commits one cp.async group per call
+// (possibly empty), so the groups of the two buffers complete in order.
 __device__ __forceinline__ int tile_stage(const XsDev &X, const XsTables &T, TileSmem &S, int b, int c0, int j1,
                                           RunSearch r) {
   const int lane = threadIdx.x & 31;
@@ -159,16 +136,22 @@ __device__ __forceinline__ int tile_stage(const XsDev &X, const XsTables &T, Til
   const bool fits = valid && incl <= (uint32_t)kCap;  // a prefix of the lanes (every valid run has >= 1 record)
   const int nsel = __popc(__ballot_sync(0xffffffffu, fits));
   const uint32_t total = __shfl_sync(0xffffffffu, incl, nsel > 0 ? nsel - 1 : 0);
-  if (lane == 0) mbar_arrive_tx(&S.bar[b], total * 128u);
-  __syncwarp();
   if (fits) {
     const uint2 e = tab_ent(T, c0 + lane, true);
     const uint32_t kb = e.x + r.klo, off = incl - cnt;
     S.meta[b][lane] = make_uint2(kb, off | (cnt << 8) | (wide << 16));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's previous generic reads
-    for (uint32_t k = 0; k < cnt; k++)  // one bulk copy per record (the SMEM stride is padded)
-      bulk_g2s(S.rec[b][off + k], X.XR + (size_t)(kb + k) * 16, 128u, &S.bar[b]);
+    for (uint32_t k = 0; k < cnt; k++) S.src[off + k] = kb + k;
   }
+  __syncwarp();
+  // the warp copies the chunk's records cooperatively, 16 B per cp.async (8 per record; a bulk copy
+  // takes uniform operands, so per-lane bulk copies serialise through an elect loop)
+  for (uint32_t q = lane; q < total * 8u; q += 32) {
+    const uint32_t rr = q >> 3, part = q & 7u;
+    const double *src = X.XR + (size_t)S.src[rr] * 16 + 2 * part;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(S.rec[b][rr] + 16 * part)), "l"(src)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   return nsel;
 }
 
@@ -184,7 +167,7 @@ __device__ __forceinline__ uint32_t run_count(const unsigned char *rec, uint32_t
 }
 
 template <int GT, bool FAST>
-__device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, TileSmem &S, uint32_t (&phase),
+__device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, TileSmem &S,
                                           const double (&E)[kL], const uint32_t (&ix)[kL], int j0, int j1,
                                           double Emin, double Emax, uint32_t imin, uint32_t imax,
                                           double (&m)[kL][5]) {
@@ -207,8 +190,10 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
   RunSearch pend = tile_search<GT>(X, T, nxt, j1, Emin, Emax, imin, imax);
   int b = 0;
   while (cs0 < j1) {
-    mbar_wait(&S.bar[b], (phase >> b) & 1u);
-    phase ^= 1u << b;
+    if (cn1 > 0)  // the next chunk's group was committed after this one's: let it stay in flight
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
 #pragma unroll 1
     for (int s = 0; s < cn0; s++) {
@@ -400,13 +385,7 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   TileSmem &S = reinterpret_cast<TileSmem *>(smem + tile_table_bytes(X.total))[warp];
-  if (lane == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  const XsTables T = stage_xs_tables<true, GT == kGridNB>(X, smem);  // (its __syncthreads publishes ms, bars)
-  uint32_t phase = 0;
+  const XsTables T = stage_xs_tables<true, GT == kGridNB>(X, smem);  // (its __syncthreads publishes ms)
   n = min(n, ms[kMats]);  // lookups kept by the sort (band grids keep their band's)
   uint32_t vacc = 0;
   const uint32_t ntiles = (n + 32 * kL - 1) / (32 * kL);
@@ -497,7 +476,7 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
         const double Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
         const uint32_t imin = __reduce_min_sync(0xffffffffu, ix[0]), imax = __reduce_max_sync(0xffffffffu, ix[kL - 1]);
         const int j0 = T.off[mt], j1 = T.off[mt + 1];
-        if (j1 > j0) tile_loop<GT, FAST>(X, T, S, phase, E, ix, j0, j1, Emin, Emax, imin, imax, m);
+        if (j1 > j0) tile_loop<GT, FAST>(X, T, S, E, ix, j0, j1, Emin, Emax, imin, imax, m);
 #pragma unroll
         for (int i = 0; i < kL; i++) {  // slot i holds lookup q; the pass finishes its active lookups
           const uint32_t q = (perm >> (4 * i)) & 15u;

@@ -30,6 +30,10 @@
 // energies), take the one-by-one path with the literal per-lookup search.
 #pragma once
 
+#ifndef GF_TILE_UNROLL
+#define GF_TILE_UNROLL 1  // nuclide-loop unroll (measured: 2 is slower, C3 2.89 -> 3.04 ms)
+#endif
+constexpr int kTileUnroll = GF_TILE_UNROLL;
 #ifndef GF_ODD_FIRST
 #define GF_ODD_FIRST 1  // hand out the tiles across material boundaries first
 #endif
@@ -195,7 +199,7 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
     else
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-#pragma unroll 1
+#pragma unroll kTileUnroll
     for (int s = 0; s < cn0; s++) {
       const int jj = cs0 + s;
       const uint2 mt = S.meta[b][s];

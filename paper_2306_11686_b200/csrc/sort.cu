@@ -167,14 +167,22 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
 
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
-// Bins per material: 2^17 for dense batches (17 M: ~18-36 lookups per fuel / water bin), fewer for
-// small ones so that the zeroing and the two scans over 12 x 2^b counters stay small next to the batch
-// (a 500 k-lookup history wave: 2^14), i.e. ~4 lookups per bin of the average material, b in [10, 17].
+// Bins per material: 2^17 from 1 M lookups (17 M: ~18-36 lookups per fuel / water bin; the tile kernel's
+// lanes want energy-adjacent lookups, so a 2.1 M shard keeps 2^17 too), fewer for small batches so that
+// the zeroing and the two scans over 12 x 2^b counters stay small next to the batch (a 500 k-lookup
+// history wave: 2^13), i.e. ~4 lookups per bin of the average material, b in [10, 17].
+static int sort_bits_override() {  // A/B override GF_SORT_BITS in [10, 17], read once per process
+  static const int v = [] {
+    const char *f = getenv("GF_SORT_BITS");
+    const int b = f ? atoi(f) : 0;
+    return (b >= 10 && b <= 17) ? b : 0;
+  }();
+  return v;
+}
+
 static int sort_bits(uint32_t n) {
-  if (const char *f = getenv("GF_SORT_BITS")) {  // A/B override, clamped to the scratch layout's [10, 17]
-    const int v = atoi(f);
-    if (v >= 10 && v <= 17) return v;
-  }
+  if (const int v = sort_bits_override()) return v;
+  if (n >= (1u << 20)) return 17;  // tile-kernel batches: the finest bins (C3 8-way shard 0.708 -> 0.681 ms)
   int b = 10;
   while (b < 17 && ((uint64_t)kMats << (b + 2)) < n) b++;
   return b;

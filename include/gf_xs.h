@@ -244,6 +244,10 @@ gf_status gf_xs_debug_set_kernel(gf_xs_grid *g, int32_t kern, uint64_t tile_min,
  * with a zero-width interval take) instead of the exact reciprocal scheme; ieee = 0 restores the
  * grid's own choice.  Results are bit-identical either way (both give the RN quotient). */
 gf_status gf_xs_debug_set_division(gf_xs_grid *g, int32_t ieee);
+/* Test hook: unionized warp-tile batches of at least n lookups (default 2^23) find each tile's union
+ * indices per tile (one pass before the lookup kernel) and search the rare leftover lookups by bisection;
+ * smaller ones use per-lookup union indices.  Identical results either way. */
+gf_status gf_xs_debug_set_prep_min(gf_xs_grid *g, uint64_t n);
 /* The sorted-path kernel (GF_KERN_*) a batch of n lookups with `flags` runs on this grid (the nuclide
  * grid reports GF_KERN_THREAD for its NB-bracket kernel); -1 for RSBench grids and unsorted batches,
  * which have one kernel each.  For reports (bench) and tests. */

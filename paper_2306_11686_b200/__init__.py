@@ -96,6 +96,7 @@ def lib():
             "gf_xs_debug_set_kernel": (i32, [vp, i32, u64, i32]),
             "gf_xs_kernel_for": (i32, [vp, u64, C.c_uint32, P(i32)]),
             "gf_xs_debug_set_division": (i32, [vp, i32]),
+            "gf_xs_debug_set_prep_min": (i32, [vp, u64]),
             "gf_xs_selftest_div": (i32, [vp, vp, vp, vp, u64, vp]),
             "gf_xs_last_error": (C.c_char_p, []),
             "gf_pr_graph_bytes": (i32, [C.c_int64, i32, P(sz), P(sz)]),
@@ -208,6 +209,10 @@ class Grid:
     def set_kernel(self, kern: str = "auto", tile_min: int = 0, nb: bool = True):
         """A/B and test hook (gf_xs_debug_set_kernel): force the sorted-path kernel of this grid."""
         _check(lib().gf_xs_debug_set_kernel(self.h, self.KERNELS[kern], tile_min, 1 if nb else 0))
+
+    def set_prep_min(self, n: int = 1 << 23):
+        """Test hook (gf_xs_debug_set_prep_min): batch size from which unionized tiles use per-tile indices."""
+        _check(lib().gf_xs_debug_set_prep_min(self.h, n))
 
     def set_ieee_division(self, ieee: bool = True):
         """Test hook (gf_xs_debug_set_division): IEEE __ddiv_rn instead of the exact reciprocal scheme."""

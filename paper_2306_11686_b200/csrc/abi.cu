@@ -247,6 +247,7 @@ static void kernel_choice(XsDev &X) {
   X.tile_min = kTileMinN;
   if (const char *m = getenv("GF_XS_TILE_MIN")) X.tile_min = (uint32_t)strtoul(m, nullptr, 10);
   X.group_min = kGroupMinN;
+  X.prep_min = 8u << 20;
   if (const char *m = getenv("GF_XS_GROUP_MIN")) X.group_min = (uint32_t)strtoul(m, nullptr, 10);
   const char *nb = getenv("GF_XS_NB");
   X.nb_on = !(nb && nb[0] == '0');
@@ -898,6 +899,13 @@ gf_status gf_xs_debug_set_division(gf_xs_grid *g, int32_t ieee) {
   if (!g) return fail(GF_E_INVAL, "grid is NULL");
   if (g->p.bench != GF_XSBENCH) return fail(GF_E_INVAL, "division choice applies to XSBench grids");
   g->xs.fastdiv = ieee ? 0 : g->fastdiv_ok;
+  return GF_OK;
+}
+
+gf_status gf_xs_debug_set_prep_min(gf_xs_grid *g, uint64_t n) {
+  if (!g) return fail(GF_E_INVAL, "grid is NULL");
+  if (g->p.bench != GF_XSBENCH) return fail(GF_E_INVAL, "applies to XSBench grids");
+  g->xs.prep_min = n >= (1ull << 32) ? 0xFFFFFFFFu : (uint32_t)n;
   return GF_OK;
 }
 

@@ -34,6 +34,10 @@
 #define GF_TILE_UNROLL 1  // nuclide-loop unroll (measured: 2 is slower, C3 2.89 -> 3.04 ms)
 #endif
 constexpr int kTileUnroll = GF_TILE_UNROLL;
+// Unionized batches from kPrepMin lookups: per-tile union indices (tile_prep) instead of per-lookup ones
+// (idx_prep), and the rare per-lookup searches by bisection (PREP).  Measured: C3 17 M 2.885 -> 2.812 ms;
+// at 2 M lookups the per-lookup searches are frequent and the per-lookup index wins (0.68 vs 0.76 ms).
+constexpr uint32_t kPrepMin = 8u << 20;  // (XsDev::prep_min: default; a test hook lowers it)
 #ifndef GF_ODD_FIRST
 #define GF_ODD_FIRST 1  // hand out the tiles across material boundaries first
 #endif
@@ -92,6 +96,24 @@ __device__ __forceinline__ void reload_rec_smem_if(uint32_t a, bool p, Rec &R) {
 }
 
 __device__ __forceinline__ long long smem_bits(const unsigned char *a) { return *reinterpret_cast<const long long *>(a); }
+
+// Record index of lookup E for table entry e by the plain bisection over the nuclide's energies
+// (= the index grid's interval; also for band grids: the absolute interval).  The
+// unionized tile kernel's rare per-lookup paths use it: they have no per-lookup union index.
+__device__ __forceinline__ uint32_t nuc_bisect_rec(const XsDev &X, uint2 e, double E) {
+  const uint32_t base = (e.y / (uint32_t)X.ig_pitch) * (uint32_t)X.n_gp;
+  int k = bisect<int>(X.Ed + base, E, 0, X.n_gp - 1);
+  return base + (uint32_t)(k == X.n_gp - 1 ? k - 1 : k);
+}
+
+// The record index of lookup E (grid index ix) for entry e, per lookup: the literal search.
+template <int GT, bool PREP>
+__device__ __forceinline__ uint32_t lookup_rec(const XsDev &X, uint2 e, double E, uint32_t ix) {
+  if (GT == GF_GRID_UNIONIZED && PREP) return nuc_bisect_rec(X, e, E);
+  long long id = ix;
+  if (GT == kGridNB) id = energy_index<kGridNB>(X, E);
+  return e.x + interval<GT>(X, e, E, id);
+}
 
 // The grid type's literal search for the tile at energy E with grid index ix (union index / hash bin;
 // kGridNB bins the energy itself).
@@ -170,7 +192,7 @@ __device__ __forceinline__ uint32_t run_count(const unsigned char *rec, uint32_t
   return c;
 }
 
-template <int GT, bool FAST>
+template <int GT, bool FAST, bool PREP>
 __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, TileSmem &S,
                                           const double (&E)[kL], const uint32_t (&ix)[kL], int j0, int j1,
                                           double Emin, double Emax, uint32_t imin, uint32_t imax,
@@ -245,10 +267,7 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
           if (!(wide && c == nbd)) {
             load_rec_smem<FAST>(ra + kRecStride * c, P);
           } else {  // beyond the staged part of a cut run: the literal search
-            const uint2 e = tab_ent(T, jj, true);
-            long long id = ix[i];
-            if (GT == kGridNB) id = energy_index<kGridNB>(X, E[i]);
-            load_rec<FAST>(X, e.x + interval<GT>(X, e, E[i], id), P);
+            load_rec<FAST>(X, lookup_rec<GT, PREP>(X, tab_ent(T, jj, true), E[i], ix[i]), P);
           }
           accumulate_rec<FAST>(P, E[i], conc, m[i]);
         }
@@ -271,7 +290,7 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
 
 // One-by-one path: lookups of a tile that straddles a material boundary or the batch end, or with
 // energies outside the tile path's domain.  The literal per-lookup search (interval<GT>).
-template <int GT, bool FAST>
+template <int GT, bool FAST, bool PREP>
 __device__ __forceinline__ void lookups_one_by_one(const XsDev &X, const XsTables &T, const uint32_t *ms,
                                                    uint32_t p0, uint32_t nl, const double (&E)[kL],
                                                    const uint32_t (&ix)[kL], double (&m)[kL][5]) {
@@ -285,12 +304,10 @@ __device__ __forceinline__ void lookups_one_by_one(const XsDev &X, const XsTable
     const int j0 = T.off[mat], j1 = T.off[mat + 1];
     double mi[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const bool fi = FAST && fabs(E[i]) <= 2.0;
-    long long id = ix[i];
-    if (GT == kGridNB) id = energy_index<kGridNB>(X, E[i]);
     for (int j = j0; j < j1; j++) {
       Rec P;
       const uint2 ej = tab_ent(T, j, true);
-      const uint32_t rec = ej.x + interval<GT>(X, ej, E[i], id);
+      const uint32_t rec = lookup_rec<GT, PREP>(X, ej, E[i], ix[i]);
       const double cj = tab_conc(T, j, true);
       if (fi) {
         load_rec<FAST>(X, rec, P);
@@ -329,13 +346,26 @@ __device__ __forceinline__ long long warp_min64(long long v) {
   return v;
 }
 
+// The union indices of lo and hi (two-level search), out of line: only the passes of the <= 13 tiles
+// across a material boundary need it in the tile kernel, whose loop registers it must not cost.
+__device__ __noinline__ uint32_t union_index(const uint32_t *ubin, const double *U, long long n_union, double E) {
+  XsDev X;  // (the two-level search reads ubin, U and n_union only)
+  X.ubin = ubin;
+  X.U = U;
+  X.n_union = n_union;
+  return (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, E);
+}
+__device__ __forceinline__ uint2 union_range(const XsDev &X, double lo, double hi) {
+  return make_uint2(union_index(X.ubin, X.U, X.n_union, lo), union_index(X.ubin, X.U, X.n_union, hi));
+}
+
 #ifndef GF_TILE_MINB
 #define GF_TILE_MINB 4
 #endif
 
 // One lane of a tile with odd energies (caller states outside [+0, 2], hash lookups on a bin edge): the
 // group kernel's pipelined loop if its 4 lookups share a material, else one by one.
-template <int GT, bool FAST>
+template <int GT, bool FAST, bool PREP>
 __device__ __forceinline__ void odd_lane(const XsDev &X, const XsTables &T, const uint32_t *ms, uint32_t p0,
                                       uint32_t nl, double (&E)[kL], uint32_t (&ix)[kL], double (&m)[kL][5],
                                       uint32_t &perm) {
@@ -345,23 +375,23 @@ __device__ __forceinline__ void odd_lane(const XsDev &X, const XsTables &T, cons
     if (p0 >= ms[mm]) lm0 = mm;
     if (p0 + nl - 1 >= ms[mm]) lm1 = mm;
   }
-  const bool fast = FAST && GT != kGridNB && nl == kL && ok_energies(E);
+  const bool fast = FAST && (GT == GF_GRID_HASH || (GT == GF_GRID_UNIONIZED && !PREP)) && nl == kL && ok_energies(E);  // (unionized: no per-lookup index)
   if (fast && lm0 == lm1) {
     local_sort(E, ix, perm);
     const int j0 = T.off[lm0], j1 = T.off[lm0 + 1];
     if (j1 > j0) group_loop<GT, FAST>(X, T, E, ix, j0, j1, m);
   } else {
-    lookups_one_by_one<GT, FAST>(X, T, ms, p0, nl, E, ix, m);
+    lookups_one_by_one<GT, FAST, PREP>(X, T, ms, p0, nl, E, ix, m);
   }
 }
 
 // The 4 sorted lookups of lane position p0 (nl of them; missing ones repeat the last, or E = 0 if none).
-template <int GT>
+template <int GT, bool PREP>
 __device__ __forceinline__ void load_tile_lookups(const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
                                                   uint32_t p0, uint32_t nl, double (&E)[kL], uint32_t (&ix)[kL]) {
   if (nl == kL) {
     asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(E[0]), "=d"(E[1]), "=d"(E[2]), "=d"(E[3]) : "l"(Es + p0));
-    if (GT != kGridNB) {
+    if (GT == GF_GRID_HASH || (GT == GF_GRID_UNIONIZED && !PREP)) {
       const uint4 v = __ldg(reinterpret_cast<const uint4 *>(ixs + p0));
       ix[0] = v.x; ix[1] = v.y; ix[2] = v.z; ix[3] = v.w;
     } else {
@@ -373,13 +403,13 @@ __device__ __forceinline__ void load_tile_lookups(const double *__restrict__ Es,
     for (int i = 0; i < kL; i++) {
       const uint32_t p = nl ? p0 + min((uint32_t)i, nl - 1) : 0u;
       E[i] = nl ? Es[p] : 0.0;
-      ix[i] = (nl && GT != kGridNB) ? ixs[p] : 0u;
+      ix[i] = (nl && (GT == GF_GRID_HASH || (GT == GF_GRID_UNIONIZED && !PREP))) ? ixs[p] : 0u;
     }
   }
 }
 
 // ix: the per-lookup grid index from idx_prep (union index / hash bin); unused for kGridNB.
-template <int GT, bool FAST>
+template <int GT, bool FAST, bool PREP>
 __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
     xs_lookup_tile(XsDev X, uint32_t n, const double *__restrict__ Es, const uint32_t *__restrict__ ixs,
                    const uint32_t *__restrict__ idx, const uint32_t *__restrict__ mstart, OutSpec out,
@@ -437,7 +467,22 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
     double E[kL];
     uint32_t ix[kL];
     bool ok = FAST;
-    load_tile_lookups<GT>(Es, ixs, p0, nl, E, ix);
+    load_tile_lookups<GT, PREP>(Es, ixs, p0, nl, E, ix);
+    // unionized: the tile's energy range and its union indices (tile_prep), for every pass
+    long long tlo = 0x7FF0000000000000ll, thi = (long long)0x8000000000000000ull;
+    uint2 tu = make_uint2(0u, 0u);
+    if (GT == GF_GRID_UNIONIZED && PREP) {
+#pragma unroll
+      for (int i = 0; i < kL; i++) {
+        if ((uint32_t)i >= nl) continue;
+        const long long b = __double_as_longlong(E[i]);
+        tlo = b < tlo ? b : tlo;
+        thi = b > thi ? b : thi;
+      }
+      tlo = warp_min64(tlo);
+      thi = warp_max64(thi);
+      tu = __ldg(reinterpret_cast<const uint2 *>(ixs) + t);
+    }
 #pragma unroll
     for (int i = 0; i < kL; i++) {
       if ((uint32_t)i >= nl) continue;
@@ -456,7 +501,7 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
 #pragma unroll
         for (int i = 0; i < kL; i++) act |= ((uint32_t)i < nl && p0 + i >= sb && p0 + i < se) ? (1u << i) : 0u;
         if (!__any_sync(0xffffffffu, act != 0u)) continue;
-        if (mt != mat0) load_tile_lookups<GT>(Es, ixs, p0, nl, E, ix);  // (not kept live across passes)
+        if (mt != mat0) load_tile_lookups<GT, PREP>(Es, ixs, p0, nl, E, ix);  // (not kept live across passes)
         // stand-in for inactive lookups: the lane's first active lookup, else the warp's smallest active energy
         long long a0 = 0x7FF0000000000000ll;
         uint32_t x0 = 0;
@@ -476,11 +521,27 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
         for (int i = 0; i < kL; i++)
 #pragma unroll
           for (int c = 0; c < 5; c++) m[i][c] = 0.0;
-        const double Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
-        const double Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
-        const uint32_t imin = __reduce_min_sync(0xffffffffu, ix[0]), imax = __reduce_max_sync(0xffffffffu, ix[kL - 1]);
+        double Emin, Emax;
+        uint32_t imin, imax;
+        if (GT == GF_GRID_UNIONIZED && PREP && mat0 == mat1) {  // one pass: the tile's range, its indices from tile_prep
+          Emin = __longlong_as_double(tlo);
+          Emax = __longlong_as_double(thi);
+          imin = tu.x;
+          imax = tu.y;
+        } else if (GT == GF_GRID_UNIONIZED && PREP) {  // a pass of a tile across a material boundary: its own range
+          Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
+          Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
+          const uint2 u = union_range(X, Emin, Emax);
+          imin = u.x;
+          imax = u.y;
+        } else {
+          Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
+          Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
+          imin = __reduce_min_sync(0xffffffffu, ix[0]);
+          imax = __reduce_max_sync(0xffffffffu, ix[kL - 1]);
+        }
         const int j0 = T.off[mt], j1 = T.off[mt + 1];
-        if (j1 > j0) tile_loop<GT, FAST>(X, T, S, E, ix, j0, j1, Emin, Emax, imin, imax, m);
+        if (j1 > j0) tile_loop<GT, FAST, PREP>(X, T, S, E, ix, j0, j1, Emin, Emax, imin, imax, m);
 #pragma unroll
         for (int i = 0; i < kL; i++) {  // slot i holds lookup q; the pass finishes its active lookups
           const uint32_t q = (perm >> (4 * i)) & 15u;
@@ -497,7 +558,7 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
 #pragma unroll
         for (int c = 0; c < 5; c++) m[i][c] = 0.0;
       uint32_t perm = 0x76543210u;
-      odd_lane<GT, FAST>(X, T, ms, p0, nl, E, ix, m, perm);
+      odd_lane<GT, FAST, PREP>(X, T, ms, p0, nl, E, ix, m, perm);
 #pragma unroll
       for (uint32_t i = 0; i < (uint32_t)kL; i++) {
         if (i < nl) {
@@ -510,16 +571,49 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
   hash_epilogue(vacc, vsum);
 }
 
-template <int GT, bool FAST>
-static cudaError_t launch_tile(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
+// A3 for the unionized tile kernel, per tile instead of per lookup: tix[t] = {u(Emin), u(Emax)}, the union
+// indices (two-level search) of the smallest and largest energy of sorted tile t (positions
+// [128 t, 128 t + 128) below n).  One warp per tile; replaces idx_prep (one search per lookup).
+__global__ void __launch_bounds__(256) tile_prep(XsDev X, uint32_t n, const double *__restrict__ Es,
+                                                 const uint32_t *__restrict__ mstart, uint2 *__restrict__ tix) {
+  n = min(n, __ldg(mstart + kMats));
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t P = t * 32 * kL;
+  if (P >= n) return;  // (warp-uniform)
+  long long lo = 0x7FF0000000000000ll, hi = (long long)0x8000000000000000ull;
+#pragma unroll
+  for (int i = 0; i < kL; i++) {
+    const uint32_t p = P + lane * kL + i;
+    if (p < n) {
+      const long long b = __double_as_longlong(__ldg(Es + p));
+      lo = b < lo ? b : lo;
+      hi = b > hi ? b : hi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long a = __shfl_xor_sync(0xffffffffu, lo, o), c = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = c > hi ? c : hi;
+  }
+  if (lane < 2) {
+    const uint32_t u = (uint32_t)energy_index<GF_GRID_UNIONIZED>(X, __longlong_as_double(lane ? hi : lo));
+    const uint32_t v = __shfl_sync(0x3u, u, 1);
+    if (lane == 0) tix[t] = make_uint2(u, v);
+  }
+}
+
+template <int GT, bool FAST, bool PREP>
+static cudaError_t launch_tile_p(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
                                unsigned long long *vsum, cudaStream_t st) {
   const size_t smem = tile_smem(X.total);
   int blocks_per_sm = 0;
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(xs_lookup_tile<GT, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+  if ((e = cudaFuncSetAttribute(xs_lookup_tile<GT, FAST, PREP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
       cudaSuccess)
     return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_tile<GT, FAST>, kTileTpb, smem)) !=
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xs_lookup_tile<GT, FAST, PREP>, kTileTpb, smem)) !=
       cudaSuccess)
     return e;
   int dev = 0, sms = 0;
@@ -528,11 +622,23 @@ static cudaError_t launch_tile(const XsDev &X, uint32_t n, const SortScratch &S,
   const uint32_t ntiles = (n + 32 * kL - 1) / (32 * kL);
   const uint32_t grid =
       max(1u, min((ntiles + kTileWarps - 1) / kTileWarps, (uint32_t)(sms * max(blocks_per_sm, 1))));
-  if (GT != kGridNB) {
+  if (GT == GF_GRID_UNIONIZED && PREP) {  // per-tile union indices (S.us holds uint2 per tile)
+    tile_prep<<<nblk((long long)ntiles * 32, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, reinterpret_cast<uint2 *>(S.us));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else if (GT != kGridNB) {  // per-lookup hash bins (the bin-interior check)
     idx_prep<GT><<<nblk(((long long)n + 3) / 4, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if ((e = cudaMemsetAsync(S.work, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
-  xs_lookup_tile<GT, FAST><<<grid, kTileTpb, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum, S.work);
+  xs_lookup_tile<GT, FAST, PREP><<<grid, kTileTpb, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum, S.work);
   return cudaGetLastError();
+}
+
+template <int GT, bool FAST>
+static cudaError_t launch_tile(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
+                               unsigned long long *vsum, cudaStream_t st) {
+  if constexpr (GT == GF_GRID_UNIONIZED) {
+    if (n >= X.prep_min) return launch_tile_p<GT, FAST, true>(X, n, S, out, vsum, st);
+  }
+  return launch_tile_p<GT, FAST, false>(X, n, S, out, vsum, st);
 }

@@ -227,6 +227,8 @@ def test_alternative_sorted_kernels_match(gf, kernel, grid):
     o = O.XSOracle(355, 11303, grid)
     g = gf.Grid(gf.Params.xsbench(355, 11303, grid))
     g.set_kernel(kernel)
+    if kernel == "tile" and grid == 1:
+        g.set_prep_min(1_000_000)  # the 2.125 M batch below takes the per-tile-index variant, 200 k the other
     for first, n in ((3_000_000, 200_000), (0, 2_125_000)):
         r1, m1 = o.lookup_batch(first, n, want_macro=True)
         r2, m2 = g.lookup_batch(first, n, want_macro=True)
@@ -352,8 +354,10 @@ def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
             Es += [e + d * 2.0 ** -40 for d in (-3, -1, 0, 1, 3)]
     Es += list(0.3 + rng.random(20000) * 1e-3)  # dense: about 20 lookups per interval per nuclide
     E = np.clip(np.array(Es), 0.0, 1.0)
-    for kern in ("auto", "tile", "group"):  # the warp-tile kernel's runs (R-TILE) see the same clusters
+    for kern, prep in (("auto", 0), ("tile", 0), ("tile", 1 << 23), ("group", 0)):  # R-TILE runs see the clusters
         g.set_kernel(kern)
+        if grid_type == 1:
+            g.set_prep_min(prep)  # 0: per-tile union indices and the bisection fallback even for this small batch
         for mat in (0, 4, 7):
             mats = np.full(len(E), mat, dtype=np.uint8)
             raw_o, m_o = o.lookup_energies(E, mats.astype(np.int32))

@@ -92,7 +92,7 @@ def launches_per_step(bench, gt, sorted_, kern=""):
     kernel; the unionized / hash tile and group kernels are preceded by idx_prep (A3)."""
     if not sorted_:
         return 1
-    return 4 + (2 if (bench == "xs" and gt in (1, 2) and kern in ("tile", "group", "")) else 1)
+    return 4 + (2 if (bench == "xs" and gt in (1, 2) and kern in ("tile", "group", "")) else 1)  # (+ tile_prep / idx_prep)
 
 
 def load_profile(cfg, sorted_):
@@ -807,10 +807,11 @@ def main():
         elif not flags:
             kname = f"xs_lookup_direct<{gname}>"
         elif gt == 0:
-            kname = ("xs_lookup_sorted<kGridNB> (per-nuclide bin brackets)" if kern == "thread"
-                     else "xs_lookup_warp_nuclide (warp-cooperative search)")
+            kname = {"thread": "xs_lookup_sorted<kGridNB> (per-nuclide bin brackets)",
+                     "tilenb": "xs_lookup_tile<nuclide grid> (warp tiles, runs from the per-nuclide bin brackets)"}.get(
+                kern, "xs_lookup_warp_nuclide (warp-cooperative search)")
         else:
-            kname = {"tile": f"xs_lookup_tile<{gname}> (warp tiles, SMEM-staged interval runs; + idx_prep)",
+            kname = {"tile": f"xs_lookup_tile<{gname}> (warp tiles, SMEM-staged interval runs; + tile_prep / idx_prep)",
                      "group": f"xs_lookup_group<{gname}> (+ idx_prep)",
                      "thread": "xs_lookup_sorted<kGridNB> (one lookup per thread)"}.get(kern, kern)
         if HL:

@@ -172,7 +172,9 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.Ed = take(npts * 8);
     L.Rd = take(npts * 8);
     L.flags = take(16);
-    if (p->grid_type != GF_GRID_NUCLIDE) L.XR = take(npts * 128 + 256);  // + the tile kernel's slot overrun
+    // interval records (+ the tile kernel's slot overrun); nuclide grids have them where the tile kernel can
+    // run on them (n_gp < 65536: the per-nuclide bin brackets find its runs)
+    if (p->grid_type != GF_GRID_NUCLIDE || p->n_gridpoints < 65536) L.XR = take(npts * 128 + 256);
     if (p->grid_type == GF_GRID_NUCLIDE && p->n_gridpoints < 65536) {  // sorted batches search NB brackets
       L.nb_pitch = ((1 << kNbLog2) + 1 + 63) & ~63;
       L.NB = take((size_t)p->n_isotopes * L.nb_pitch * 2);
@@ -401,7 +403,7 @@ gf_status gf_xs_grid_init(const gf_xs_params *p, int device, void *grid_mem, siz
       double *Ed = reinterpret_cast<double *>(base + L.Ed);
       double *Rd = reinterpret_cast<double *>(base + L.Rd);
       int *zero_width = reinterpret_cast<int *>(base + L.flags);
-      double *XR = X.grid_type != GF_GRID_NUCLIDE ? reinterpret_cast<double *>(base + L.XR) : nullptr;
+      double *XR = L.XR ? reinterpret_cast<double *>(base + L.XR) : nullptr;
       double *U = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<double *>(base + L.U) : nullptr;
       uint16_t *IG = X.grid_type == GF_GRID_UNIONIZED ? reinterpret_cast<uint16_t *>(base + L.IG) : nullptr;
       uint16_t *HG = X.grid_type == GF_GRID_HASH ? reinterpret_cast<uint16_t *>(base + L.HG) : nullptr;
@@ -915,8 +917,11 @@ gf_status gf_xs_kernel_for(const gf_xs_grid *g, uint64_t n, uint32_t flags, int3
   if (g->p.bench != GF_XSBENCH || !(flags & GF_SORT_LOCALITY)) return GF_OK;  // RS / unsorted: one kernel each
   const XsDev &X = g->xs;
   if (X.grid_type == GF_GRID_NUCLIDE) {
-    *kern = (X.NB && X.nb_on && X.kern != kKernWarpSearch) ? GF_KERN_THREAD
-            : (X.kern == kKernThread ? GF_KERN_THREAD : GF_KERN_WARP_SEARCH);
+    const bool tile = X.XR && X.NB && (X.kern == kKernTile || X.kern == kKernTileNB ||
+                                       (X.kern == kKernAuto && n >= X.tile_min));
+    *kern = tile ? GF_KERN_TILE_NB
+                 : (X.NB && X.nb_on && X.kern != kKernWarpSearch) ? GF_KERN_THREAD
+                 : (X.kern == kKernThread ? GF_KERN_THREAD : GF_KERN_WARP_SEARCH);
     return GF_OK;
   }
   *kern = X.kern != kKernAuto ? X.kern : (n >= X.tile_min ? GF_KERN_TILE : n >= X.group_min ? GF_KERN_GROUP : GF_KERN_THREAD);

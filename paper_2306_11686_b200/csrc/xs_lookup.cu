@@ -431,6 +431,11 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
         return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st)
                          : launch_tile<kGridNB, false>(X, n, S, out, vsum, st);
     }
+    if constexpr (GT == GF_GRID_NUCLIDE) {  // the warp-tile kernel with runs from the NB brackets
+      if ((kern == kKernTile || kern == kKernTileNB) && X.XR && X.NB)
+        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st)
+                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st);
+    }
     if (GT == GF_GRID_NUCLIDE && X.NB && X.nb_on && kern != kKernWarpSearch) {
       if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;
       xs_lookup_sorted<kGridNB><<<nblk(n, kLookupTpb), kLookupTpb, smem, st>>>(X, n, S.Es, S.idx, S.mstart, out,

@@ -111,9 +111,8 @@ def test_grid_bytes_closed_form():
             pitch = (npts + 63) // 64 * 64
             want += al(npts * 8) + al(n_iso * pitch * 2) + al((2 ** 20 + 1) * 4)
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts (sparse batches)
-        if gt != gf.NUCLIDE:
-            want += al(npts * 128 + 256)  # interval records of the sorted kernels (+ 2 records of tile-slot overrun)
-        else:
+        want += al(npts * 128 + 256)  # interval records of the sorted kernels (+ 2 records of tile-slot overrun)
+        if gt == gf.NUCLIDE:
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts
         if gt == gf.HASH:
             want += al(n_iso * 10048 * 2)

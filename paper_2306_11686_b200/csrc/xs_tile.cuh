@@ -97,6 +97,29 @@ __device__ __forceinline__ void reload_rec_smem_if(uint32_t a, bool p, Rec &R) {
 
 __device__ __forceinline__ long long smem_bits(const unsigned char *a) { return *reinterpret_cast<const long long *>(a); }
 
+// Shared-memory loads by 32-bit address, not volatile (the compiler may schedule them freely): every
+// address is derived from the token the cp.async wait returns, so none can move above the wait.
+__device__ __forceinline__ long long lds64(uint32_t a) {
+  long long v;
+  asm("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+template <bool FAST>
+__device__ __forceinline__ void lds_rec(uint32_t a, Rec &R) {
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(R.v0.x), "=d"(R.v0.y) : "r"(a));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2 + 16];" : "=d"(R.v1.x), "=d"(R.v1.y) : "r"(a));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2 + 32];" : "=d"(R.v2.x), "=d"(R.v2.y) : "r"(a));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2 + 48];" : "=d"(R.v3.x), "=d"(R.v3.y) : "r"(a));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2 + 64];" : "=d"(R.v4.x), "=d"(R.v4.y) : "r"(a));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2 + 80];" : "=d"(R.v5.x), "=d"(R.v5.y) : "r"(a));
+  if (FAST) asm("ld.shared.f64 %0, [%1 + 96];" : "=d"(R.y) : "r"(a));
+}
+
 // Record index of lookup E for table entry e by the plain bisection over the nuclide's energies
 // (= the index grid's interval; also for band grids: the absolute interval).  The
 // unionized tile kernel's rare per-lookup paths use it: they have no per-lookup union index.
@@ -184,11 +207,11 @@ __device__ __forceinline__ int tile_stage(const XsDev &X, const XsTables &T, Til
 // #{m < nbd : boundary m <= E}, the boundaries being the first doubles of the records at `rec` (kRecStride
 // stride, sorted): a branch-free binary search whose steps depend on nbd only (warp-uniform).  Bit
 // patterns of non-negative doubles order as signed 64-bit integers.
-__device__ __forceinline__ uint32_t run_count(const unsigned char *rec, uint32_t nbd, long long eb) {
+__device__ __forceinline__ uint32_t run_count(uint32_t rec, uint32_t nbd, long long eb) {
   uint32_t c = 0;
   if (nbd == 0) return 0;
   for (uint32_t step = 1u << (31 - __clz(nbd)); step; step >>= 1)
-    if (c + step <= nbd && eb >= smem_bits(rec + kRecStride * (c + step - 1))) c += step;
+    if (c + step <= nbd && eb >= lds64(rec + kRecStride * (c + step - 1))) c += step;
   return c;
 }
 
@@ -216,35 +239,37 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
   RunSearch pend = tile_search<GT>(X, T, nxt, j1, Emin, Emax, imin, imax);
   int b = 0;
   while (cs0 < j1) {
+    uint32_t tok;  // 0, produced after the wait: the chunk's shared addresses depend on it
     if (cn1 > 0)  // the next chunk's group was committed after this one's: let it stay in flight
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n mov.u32 %0, 0;" : "=r"(tok) :: "memory");
     else
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n mov.u32 %0, 0;" : "=r"(tok) :: "memory");
     __syncwarp();
+    const uint32_t mb = smem_u32(&S.meta[b][0]) + tok, rb = smem_u32(&S.rec[b][0][0]) + tok;
 #pragma unroll kTileUnroll
     for (int s = 0; s < cn0; s++) {
       const int jj = cs0 + s;
-      const uint2 mt = S.meta[b][s];
+      const uint2 mt = lds_u2(mb + 8u * (uint32_t)s);
       const uint32_t off = mt.y & 0xFFu, cnt = (mt.y >> 8) & 0xFFu;
       const bool wide = (mt.y >> 16) != 0u;
-      const unsigned char *ra = S.rec[b][off];
+      const uint32_t ra = rb + kRecStride * off;  // shared address of the run's first record
       const uint32_t nbd = cnt - 1u;  // staged boundaries A[klo + 1 .. klo + cnt - 1]
       // lookup 0 by a binary search over the run; the thread's other lookups (a much narrower range)
       // against the next three boundaries: c_i = ca + [E_i >= bx] + [E_i >= by] while E_i < bz
       const uint32_t ca = run_count(ra, nbd, eb[0]);
       const long long kInf = 0x7FF0000000000000ll;  // (+inf: no boundary)
-      const long long bx = ca < nbd ? smem_bits(ra + kRecStride * ca) : kInf;
-      const long long by = ca + 1u < nbd ? smem_bits(ra + kRecStride * (ca + 1u)) : kInf;
-      const long long bz = ca + 2u < nbd ? smem_bits(ra + kRecStride * (ca + 2u)) : kInf;
+      const long long bx = ca < nbd ? lds64(ra + kRecStride * ca) : kInf;
+      const long long by = ca + 1u < nbd ? lds64(ra + kRecStride * (ca + 1u)) : kInf;
+      const long long bz = ca + 2u < nbd ? lds64(ra + kRecStride * (ca + 2u)) : kInf;
       const uint32_t cd = ca + (eb[kL - 1] >= bx ? 1u : 0u) + (eb[kL - 1] >= by ? 1u : 0u);
       const double conc = tab_conc(T, jj, true);
       Rec P;
       // common case: no lookup of the warp beyond a cut run, and no thread's lookups span more than two
       // boundaries (E_3 < bz)
       if (!__any_sync(0xffffffffu, (wide && cd == nbd) || eb[kL - 1] >= bz)) {
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(ra);
+        const uint32_t sa = ra;
         uint32_t cP = ca;
-        load_rec_smem<FAST>(ra + kRecStride * ca, P);
+        lds_rec<FAST>(ra + kRecStride * ca, P);
         if (!__any_sync(0xffffffffu, ca != cd)) {  // no thread straddles: the 4 chains interleave
 #pragma unroll
           for (int i = 0; i < kL; i++) accumulate_rec<FAST>(P, E[i], conc, m[i]);
@@ -265,7 +290,7 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
         for (int i = 0; i < kL; i++) {
           const uint32_t c = run_count(ra, nbd, eb[i]);
           if (!(wide && c == nbd)) {
-            load_rec_smem<FAST>(ra + kRecStride * c, P);
+            lds_rec<FAST>(ra + kRecStride * c, P);
           } else {  // beyond the staged part of a cut run: the literal search
             load_rec<FAST>(X, lookup_rec<GT, PREP>(X, tab_ent(T, jj, true), E[i], ix[i]), P);
           }

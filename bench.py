@@ -535,6 +535,11 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong (default): the config's lookups are split over the ranks (SURVEY.md 8(e)); "
                          "weak: every rank runs the config's lookups (global indices [r n, (r+1) n))")
+    ap.add_argument("--split", default="auto", choices=["auto", "index", "band"],
+                    help="strong split: index = rank r takes global lookups [r n / N, (r+1) n / N) on a replicated "
+                         "grid; band = rank r holds energy band r of N of the unionized grid and takes the batch's "
+                         "lookups in it (SURVEY.md 8(e) 'Alternative: energy-band sharding'); auto = band for "
+                         "unionized event configs, index otherwise")
     ap.add_argument("--no-proxy", action="store_true", help="skip the N=1 strong-scaling proxies (W = 2, 4, 8)")
     ap.add_argument("--no-sort", action="store_true", help="skip the A2 locality sort (unsorted gather kernel)")
     ap.add_argument("--hist-mode", default="sorted", choices=["sorted", "waves", "direct"],
@@ -598,14 +603,21 @@ def main():
         n_total = n * world
     else:
         first, n = gf.shard_range(n_total, rank, world)
+    band_ok = bench == "xs" and gt == gf.UNIONIZED and not HL and not args.no_sort
+    split = ("band" if band_ok else "index") if args.split == "auto" else args.split
+    if split == "band" and not band_ok:
+        raise SystemExit(f"--split band needs a sorted unionized event config, not {args.config}")
+    banded = split == "band" and args.scaling == "strong" and world > 1
+    if banded:  # every rank samples the whole batch; its band grid keeps the lookups in its band
+        first, n = 0, n_total
     st = torch.cuda.current_stream()
 
     # ---------------------------------------------------------------- A0: grid build (untimed)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     n_gp = 238847 if args.config == "C6" else 11303
-    params = (gf.Params.xsbench(n_iso, n_gp, gt, 10000) if bench == "xs"
-              else gf.Params.rsbench(n_iso, doppler=0 if args.config == "C5D0" else 1))
+    params = (gf.Params.xsbench(n_iso, n_gp, gt, 10000, n_bands=world if banded else 1, band=rank if banded else 0)
+              if bench == "xs" else gf.Params.rsbench(n_iso, doppler=0 if args.config == "C5D0" else 1))
     grid = gf.Grid(params, device=dev)
     e1.record()
     torch.cuda.synchronize()
@@ -737,6 +749,39 @@ def main():
                              "shard_ms": [round(x, 4) for x in shard_ms], "hash": gf.verify(raw_w)}
         proxy["note"] = ("per-rank step (sort + lookup) of the W-way strong split, each shard timed on this GPU; "
                          "speedup = T1 / slowest shard (excludes the 8-B all-reduce)")
+    # The energy-band split (--split band, the default for unionized event configs at N > 1): every band
+    # replica r of W is built in turn on this GPU (build untimed) and runs the whole batch, its sort keeping
+    # the lookups in band r; the slowest band bounds a W-GPU step.
+    proxy_band = None
+    if proxy is not None and band_ok:
+        T1 = tot_ms / K
+        proxy_band = {"T1_ms": T1}
+        for W in (2, 4, 8):
+            band_ms, raw_w = [], 0
+            for r in range(W):
+                gb = gf.Grid(gf.Params.xsbench(n_iso, n_gp, gt, 10000, n_bands=W, band=r), device=dev)
+                ts = []
+                for k in range(4):  # 1 warm-up + 3 timed
+                    flush.fill_(k & 0xFF)
+                    vsum.zero_()
+                    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    p0.record()
+                    gf._check(L.gf_xs_lookup_batch(gb.h, 0, n_total, gf.STARTING_SEED, flags, None,
+                                                   C.c_void_p(vsum.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                                   scratch.numel(), C.c_void_p(st.cuda_stream)))
+                    p1.record()
+                    torch.cuda.synchronize()
+                    if k:
+                        ts.append(p0.elapsed_time(p1))
+                raw_w += int(vsum.item())
+                band_ms.append(statistics.median(ts))
+                gb.close()
+            mx = max(band_ms)
+            proxy_band[str(W)] = {"lookups_per_rank": n_total // W, "max_band_ms": mx, "speedup": T1 / mx,
+                                  "band_ms": [round(x, 4) for x in band_ms], "hash": gf.verify(raw_w)}
+        proxy_band["note"] = ("per-rank step (sort of the whole batch keeping band r, lookup of its ~n/W lookups on "
+                              "the band-r grid replica) of the W-way energy-band split, each band timed on this GPU; "
+                              "speedup = T1 / slowest band (excludes the 8-B all-reduce)")
 
     # ---------------------------------------------------------------- end-to-end through the public API
     e2e = None
@@ -757,6 +802,19 @@ def main():
         e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
                "path": "Grid.history_batch (gf_xs_history_batch): particle indices + seed in, raw sum (8 B) out; "
                        "host-timed incl. launch and sync"}
+    elif not args.no_e2e and banded:  # band grids take sampled lookups only: indices + seed in, raw sum out
+        reps = 3
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r_e2e = grid.lookup_batch(first, n)
+            rt = torch.tensor([r_e2e], dtype=torch.int64, device=dev)
+            gdist.reduce_raw(rt)
+        el = gdist.max_over_ranks([time.perf_counter() - t0], dev)[0]
+        e2e = {"value": n_total * reps / el, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
+               "path": "Grid.lookup_batch (gf_xs_lookup_batch) on the rank's band grid: batch indices + seed in, "
+                       "raw sum (8 B) out; host-timed incl. launch and sync (band grids take no caller energies)"}
     elif not args.no_e2e:
         import numpy as np
         rng = np.random.default_rng(1234 + rank)
@@ -798,7 +856,8 @@ def main():
     if rank == 0:
         peaks = load_peaks()
         alg_bytes, alg_flops = ALG[args.config]
-        per_launch_lookups = n  # one lookup-kernel launch per step per rank
+        # one lookup-kernel launch per step per rank (a band rank's launch covers its band's lookups, n / N expected)
+        per_launch_lookups = n_total // world if banded else n
         look_avg_s = look_tot / K * 1e-3
         gname = {0: "nuclide", 1: "unionized", 2: "hash"}.get(gt, "")
         kern = grid.kernel_for(n, flags) if (bench == "xs" and not HL) else ""
@@ -860,16 +919,21 @@ def main():
             "metric": "lookups/sec", "value": value, "unit": "lookups/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
-            "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n,
+            "config": {"workload": f"{args.config}: {desc}", "n_lookups": n_total, "lookups_per_rank": n_total // world if banded else n,
                        **({"mode": f"history ({args.hist_mode})", "particles_per_rank": n_part,
                            "launch": "one CUDA graph of the gf_xs_history_batch call, replayed per step"
                            if graph is not None else "direct",
                            "lookups_per_particle": HL} if HL else {}),
                        "sort": not args.no_sort, "l2": "flushed between steps by a 256 MiB write (outside events)",
-                       "parallelism": f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, {first + n}) on rank 0), "
-                                      f"grid replicated, 1 int64 "
-                                      f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
-            "roofline": roof, "rho": rho, "strong_proxy": proxy, "paper_context": paper,
+                       "split": split if world > 1 else None,
+                       "parallelism": (f"strong-scaled energy bands x{world} (rank 0: band [0, 1/{world}) of the "
+                                       f"unionized grid, all {n_total} lookups sampled, its band's kept), 1 int64 "
+                                       if banded else
+                                       f"{args.scaling}-scaled lookup shards x{world} (global indices [{first}, "
+                                       f"{first + n}) on rank 0), grid replicated, 1 int64 ")
+                                      + f"{os.environ.get('GF_DIST_BACKEND', 'nccl').upper()} all-reduce/step"},
+            "roofline": roof, "rho": rho, "strong_proxy": proxy, "strong_proxy_band": proxy_band,
+            "paper_context": paper,
             "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY, kern) if not HL else
                                  (1 if args.hist_mode == "direct" else

@@ -216,7 +216,7 @@ static gf_status plan(const gf_xs_params *p, int total, Layout &L) {
     L.woff = take((n + 1) * 4);
     L.scratch_bytes = al(2 * n * 4);
   }
-  L.thr = take(32 * 8);  // T[12] doubles, then the integer thresholds S[12] (u64)
+  L.thr = take(kThrBytes);  // T[12] doubles, the integer thresholds S[12] (u64), the sampling tables
   L.moff = take(16 * 4);
   L.mnuc = take((size_t)(total > 0 ? total : 1) * 4);
   L.mconc = take((size_t)(total > 0 ? total : 1) * 8);

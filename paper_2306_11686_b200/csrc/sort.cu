@@ -13,39 +13,74 @@
 #include "gf_internal.cuh"
 
 #include <cstdlib>
+#include <algorithm>
 #include <cmath>
 
 namespace gf {
 
 constexpr int kRun = 16;   // sort_scatter: lookups per thread (registers hold them between phases)
 constexpr int kRunC = 16;  // sort_count: lookups per thread (64 measured: no faster at 17 M, slower for small batches)
+constexpr int kSampTpb = 256;
+static_assert(kRun == 16 && kRunC == 16 && kSampTpb == 256, "the offset maps (kOffMapOff) are for 256 x 16 lookups");
+
+// A sampling CTA (kSampTpb threads x 16 consecutive lookups): the integer thresholds and the material
+// bucket table go to shared memory; thread 0 skips to the CTA's first lookup once (gen: sampled, not
+// caller, energies) and every thread starts from it through the offset map of its 32 t steps -- one
+// affine map instead of a ~25-step skip per thread.
+struct SampleSmem {
+  unsigned long long sT[kMats];
+  unsigned long long base;
+  alignas(16) uint8_t tab[1 << kMatTabLog2];
+};
+__device__ __forceinline__ void stage_sampler(SampleSmem &Q, const double *thr, uint64_t first, uint64_t seed,
+                                              bool gen) {
+  const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
+  if (threadIdx.x < kMats) Q.sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
+  reinterpret_cast<uint4 *>(Q.tab)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(tb + kMatTabOff) + threadIdx.x);
+  if (gen && threadIdx.x == 0) Q.base = lcg_skip(seed, 2ull * (first + (uint64_t)blockIdx.x * kSampTpb * kRun));
+  __syncthreads();
+}
+__device__ __forceinline__ uint64_t thread_start(const double *thr, const SampleSmem &Q) {
+  const ulonglong2 m =
+      __ldg(reinterpret_cast<const ulonglong2 *>(reinterpret_cast<const unsigned char *>(thr) + kOffMapOff) + threadIdx.x);
+  return (m.x * Q.base + m.y) & kLcgMask;
+}
 
 // Band filter of a NEXT-2 band grid: [lo, hi).  The defaults (-inf, +inf) mean "no band" and keep
 // every lookup, +-inf and NaN energies included.
-// Sort bin of E within its material with 2^nb_log2 bins: floor(E 2^nb_log2) clamped (exact scaling).
-__device__ __forceinline__ int sort_bin_bits(double E, int nb_log2) {
-  int b = (int)__dmul_rn(E, (double)(1 << nb_log2));
+// Sort bins within a material: 2^nbl bins, bin = floor((E - b0) 2^sl) clamped (a whole grid: b0 = 0,
+// sl = nbl, exact scaling).  A band grid's batch covers only its band [b0, b0 + 1/W): its bins span the
+// band at the whole grid's density (sl = nbl + floor(log2 W)), so the zeroing and the scans shrink W-fold.
+// Sampled lookups are filtered on the LCG state instead: E = RN(s) 2^-63 is non-decreasing in s, so
+// band_lo <= E < band_hi exactly when slo <= s < shi (state_threshold), and a lookup outside the band
+// costs its two LCG steps and two compares only.
+struct SortBins {
+  double b0;
+  int sl, nbl;
+  unsigned long long slo, shi;  // the band on the LCG state (whole grid: 0, 2^63)
+};
+__device__ __forceinline__ int sort_bin(double E, const SortBins &B) {
+  int b = (int)__dmul_rn(__dsub_rn(E, B.b0), (double)(1 << B.sl));
   b = b < 0 ? 0 : b;
-  return b > (1 << nb_log2) - 1 ? (1 << nb_log2) - 1 : b;
+  return b > (1 << B.nbl) - 1 ? (1 << B.nbl) - 1 : b;
 }
 
 __device__ __forceinline__ bool in_band(double E, double lo, double hi) {
   const bool whole = lo == -__longlong_as_double(0x7ff0000000000000ll) && hi == __longlong_as_double(0x7ff0000000000000ll);
   return whole || (E >= lo && E < hi);
 }  // consecutive lookups per thread in the sampling kernels
-__global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, uint64_t seed,
+__global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t n, uint64_t seed,
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
-                                                  double band_lo, double band_hi, int nb_log2,
+                                                  double band_lo, double band_hi, SortBins B,
                                                   unsigned long long *__restrict__ flag) {
-  __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
-  if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
-  __syncthreads();
+  __shared__ SampleSmem Q;
+  stage_sampler(Q, thr, first, seed, !src_E);
   uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRunC;
   if (t0 >= n) return;
   uint64_t s = 0;
-  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
+  if (!src_E) s = thread_start(thr, Q);
   for (int r = 0; r < kRunC; r++) {
     uint64_t t = t0 + r;
     if (t >= n) break;
@@ -56,12 +91,15 @@ __global__ void __launch_bounds__(256) sort_count(uint64_t first, uint32_t n, ui
       mat = src_mat[t];
       if (mat >= kMats || !isfinite(E)) invalid_input(flag);  // outside the input domain: flagged
       mat = mat < kMats ? mat : kMats - 1;
+      if (!in_band(E, band_lo, band_hi)) continue;
     } else {
-      E = lcg_draw(s);
-      s = lcg_next(s);
-      mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
+      const uint64_t s1 = lcg_next(s);
+      s = lcg_next(s1);
+      if (s1 < B.slo || s1 >= B.shi) continue;  // outside the band
+      E = lcg_unit(s1);
+      mat = pick_material_tab(s, Q.tab, Q.sT);  // == pick_material(RN(s) 2^-63, T), exact
     }
-    if (in_band(E, band_lo, band_hi)) atomicAdd(counts + (mat << nb_log2) + sort_bin_bits(E, nb_log2), 1u);
+    atomicAdd(counts + (mat << B.nbl) + sort_bin(E, B), 1u);
   }
 }
 
@@ -118,20 +156,19 @@ __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ curs
   if ((b & ((1 << nb_log2) - 1)) == 0) mstart[b >> nb_log2] = v;
 }
 
-__global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
+__global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
                                                     const double *__restrict__ src_E,
                                                     const uint8_t *__restrict__ src_mat,
                                                     const double *__restrict__ thr, uint32_t *__restrict__ cursor,
                                                     double *__restrict__ Es, uint32_t *__restrict__ idx,
-                                                    double band_lo, double band_hi, int nb_log2) {
-  __shared__ unsigned long long sT[kMats];  // integer thresholds S[m] (thresholds_kernel)
-  if (threadIdx.x < kMats) sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
-  __syncthreads();
+                                                    double band_lo, double band_hi, SortBins B) {
+  __shared__ SampleSmem Q;
+  stage_sampler(Q, thr, first, seed, !src_E);
   uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
   const int cnt = (int)min((uint64_t)kRun, n - t0);
   uint64_t s = 0;
-  if (!src_E) s = lcg_skip(seed, 2ull * (first + t0));
+  if (!src_E) s = thread_start(thr, Q);
   // three phases so that the kRun cursor atomics (each an L2 round trip) are in flight together
   double E[kRun];
   uint32_t pos[kRun];
@@ -139,18 +176,21 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
   for (int r = 0; r < kRun; r++) {
     if (r < cnt) {
       const uint64_t t = t0 + r;
-      int mat;
+      pos[r] = 0xFFFFFFFFu;  // (outside the band: dropped)
       if (src_E) {
         E[r] = src_E[t];
-        mat = src_mat[t];
+        int mat = src_mat[t];
         mat = mat < kMats ? mat : kMats - 1;
+        if (in_band(E[r], band_lo, band_hi)) pos[r] = (uint32_t)((mat << B.nbl) + sort_bin(E[r], B));
       } else {
-        E[r] = lcg_draw(s);
-        s = lcg_next(s);
-        mat = pick_material_state(s, sT);  // == pick_material(RN(s) 2^-63, T), exact
+        const uint64_t s1 = lcg_next(s);
+        s = lcg_next(s1);
+        if (s1 >= B.slo && s1 < B.shi) {
+          E[r] = lcg_unit(s1);
+          const int mat = pick_material_tab(s, Q.tab, Q.sT);  // == pick_material(RN(s) 2^-63, T), exact
+          pos[r] = (uint32_t)((mat << B.nbl) + sort_bin(E[r], B));
+        }
       }
-      pos[r] = in_band(E[r], band_lo, band_hi) ? (uint32_t)((mat << nb_log2) + sort_bin_bits(E[r], nb_log2))
-                                               : 0xFFFFFFFFu;
     }
   }
 #pragma unroll
@@ -158,7 +198,7 @@ __global__ void __launch_bounds__(256) sort_scatter(uint64_t first, uint32_t n, 
     if (r < cnt && pos[r] != 0xFFFFFFFFu) pos[r] = atomicAdd(cursor + pos[r], 1u);
 #pragma unroll
   for (int r = 0; r < kRun; r++) {
-    if (r < cnt && pos[r] != 0xFFFFFFFFu) {  // (outside the band: dropped)
+    if (r < cnt && pos[r] != 0xFFFFFFFFu) {
       Es[pos[r]] = E[r];
       if (idx) idx[pos[r]] = (uint32_t)(t0 + r);
     }
@@ -188,6 +228,34 @@ static int sort_bits(uint32_t n) {
   return b;
 }
 
+// The bins of an n-lookup batch on a grid with band [lo, hi) ((-inf, inf): whole grid; band 0 is open
+// below, the last band above, their lookups still lie in [0, 1/W) / [(W-1)/W, 1)).
+// min{s in [0, 2^63] : RN(s) 2^-63 >= T} (2^63: none), by bisection with the samplers' conversion (the
+// host's int64 -> double conversion rounds to nearest like __ull2double_rn; the scaling is exact).
+static unsigned long long state_threshold(double T) {
+  unsigned long long lo = 0ull, hi = 1ull << 63;
+  while (lo < hi) {
+    const unsigned long long mid = lo + ((hi - lo) >> 1);
+    if ((double)(long long)mid * 0x1p-63 >= T) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+static SortBins whole_bins(int nb) { return SortBins{0.0, nb, nb, 0ull, 1ull << 63}; }
+
+static SortBins sort_bins(uint32_t n, double lo, double hi) {
+  const int nb = sort_bits(n);
+  const bool flo = std::isfinite(lo), fhi = std::isfinite(hi);
+  if (!flo && !fhi) return whole_bins(nb);
+  const double width = (flo && fhi) ? hi - lo : (fhi ? hi : 1.0 - lo);
+  const long W = width > 0.0 ? std::lround(1.0 / width) : 1;
+  int wl = 0;  // floor(log2 W)
+  while (wl < 20 && (2l << wl) <= W) wl++;
+  const int nbl = nb - wl < 10 ? 10 : nb - wl;
+  return SortBins{flo ? lo : 0.0, nbl + wl, nbl, flo ? state_threshold(lo) : 0ull,
+                  fhi ? state_threshold(hi) : 1ull << 63};
+}
+
 cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) {
   return cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * (kMats << sort_bits(n)), st);
 }
@@ -197,8 +265,9 @@ cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) 
 cudaError_t launch_sort_count(uint32_t n_total, uint32_t cn, const double *src_E, const uint8_t *src_mat,
                               const double *thr, const SortScratch &S, unsigned long long *flag, cudaStream_t st) {
   const double inf = HUGE_VAL;
-  const unsigned gc = nblk(((long long)cn + kRunC - 1) / kRunC, 256);
-  sort_count<<<gc, 256, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, sort_bits(n_total), flag);
+  const unsigned gc = nblk(((long long)cn + kRunC - 1) / kRunC, kSampTpb);
+  const int nb = sort_bits(n_total);
+  sort_count<<<gc, kSampTpb, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, whole_bins(nb), flag);
   return cudaGetLastError();
 }
 
@@ -206,21 +275,22 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
                                  unsigned long long *flag, cudaStream_t st, double band_lo, double band_hi) {
   cudaError_t e;
-  const int nbl = sort_bits(n);
+  const SortBins B = S.counted ? whole_bins(sort_bits(n)) : sort_bins(n, band_lo, band_hi);
+  const int nbl = B.nbl;
   const int bins = kMats << nbl;  // a multiple of kScanBlk for nbl >= 10
-  const unsigned g = nblk(((long long)n + kRun - 1) / kRun, 256);
+  const unsigned g = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
   if (!S.counted) {
     if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
-    const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, 256);
-    sort_count<<<gc, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, nbl, flag);
+    const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, kSampTpb);
+    sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, B, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, nbl);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  sort_scatter<<<g, 256, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr,
-                                band_lo, band_hi, nbl);
+  sort_scatter<<<g, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr,
+                                band_lo, band_hi, B);
   return cudaGetLastError();
 }
 

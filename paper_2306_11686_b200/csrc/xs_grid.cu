@@ -46,8 +46,30 @@ __global__ void thresholds_kernel(double *thr) {
   }
 }
 
+// The sampling tables after the thresholds (gf_internal.cuh, kMatTabOff / kOffMapOff): one thread per
+// material-table bucket, the first 256 threads also write the offset maps.
+__global__ void __launch_bounds__(256) sample_tables_kernel(double *thr) {
+  const unsigned long long *S = reinterpret_cast<const unsigned long long *>(thr) + kMats;
+  unsigned char *base = reinterpret_cast<unsigned char *>(thr);
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < (1u << kMatTabLog2)) {
+    const unsigned long long lo = (unsigned long long)k << (63 - kMatTabLog2);
+    const unsigned long long hi = lo + (1ull << (63 - kMatTabLog2));
+    bool inside = false;
+    for (int m = 1; m < kMats; m++) inside = inside || (S[m] > lo && S[m] < hi);
+    base[kMatTabOff + k] = inside ? 0xFF : (unsigned char)pick_material_state(lo, S);
+  }
+  if (k < 256) {
+    uint64_t A, C;
+    lcg_skip_map(32ull * k, A, C);
+    reinterpret_cast<unsigned long long *>(base + kOffMapOff)[2 * k] = A;
+    reinterpret_cast<unsigned long long *>(base + kOffMapOff)[2 * k + 1] = C;
+  }
+}
+
 cudaError_t launch_tables(const double *, double *thr, cudaStream_t st) {
   thresholds_kernel<<<1, 32, 0, st>>>(thr);
+  sample_tables_kernel<<<(1u << kMatTabLog2) / 256, 256, 0, st>>>(thr);
   return cudaGetLastError();
 }
 

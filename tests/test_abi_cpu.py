@@ -116,7 +116,8 @@ def test_grid_bytes_closed_form():
             want += al(n_iso * ((2 ** 14 + 1 + 63) // 64 * 64) * 2)  # per-nuclide bin counts
         if gt == gf.HASH:
             want += al(n_iso * 10048 * 2)
-        want += al(128) + al(64) + al(total * 4) + al(total * 8)
+        # thresholds T, S + the samplers' material-bucket table (4 KB) and offset maps (4 KB); material tables
+        want += al(256 + 4096 + 4096) + al(64) + al(total * 4) + al(total * 8)
         assert gb == want, (n_iso, gt)
     # C3: the 355 x 4,012,565 u16 index grid (2.85 GB) dominates the 3.67 GB total (incl. 11.6 MB of per-nuclide bin counts)
     st, gb, _ = _bytes(gf.Params.xsbench(355, 11303, gf.UNIONIZED))

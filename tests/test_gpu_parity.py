@@ -741,23 +741,30 @@ def test_nuclide_bin_search_sparse_batches(gf, torch, n_iso, grid_type):
         assert raw_g == raw_o and np.array_equal(m_g.cpu().numpy(), m_o), flag
 
 
-@pytest.mark.parametrize("config,hash_", [("C3", 113528), ("C5", 662460)])
-def test_torchrun_two_ranks_strong_split(gf, config, hash_):
+@pytest.mark.parametrize("config,split,hash_", [("C3", "index", 113528), ("C3", "band", 113528),
+                                                ("C5", "index", 662460)])
+def test_torchrun_two_ranks_strong_split(gf, config, split, hash_):
     """The product's N > 1 path end to end: bench.py under torchrun with 2 ranks (gloo, both on this one
-    GPU: GF_DIST_BACKEND), strong split of the config's lookups, one int64
-    all-reduce of the raw sums per step -- the all-reduced hash must be the full batch's golden hash."""
+    GPU: GF_DIST_BACKEND), strong split of the config's lookups (index ranges on a
+    replicated grid, or energy bands: rank r builds band r of the unionized grid and keeps the batch's
+    lookups in it), one int64 all-reduce of the raw sums per step -- the all-reduced hash must be the full
+    batch's golden hash (the band run also runs its end-to-end leg)."""
     import subprocess
     import sys
     env = dict(os.environ, GF_DIST_BACKEND="gloo", PYTHONPATH=os.path.dirname(HERE))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(os.path.dirname(HERE), "bench.py"),
-           "--gpus", "2", "--config", config, "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+           "--gpus", "2", "--config", config, "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--split", split]
+    if split == "index":
+        cmd.append("--no-e2e")
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stderr[-3000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["config"]["lookups_per_rank"] * 2 in (
         line["config"]["n_lookups"], line["config"]["n_lookups"] + 1)
-    assert line["hash"] == hash_
+    assert line["hash"] == hash_ and line["config"]["split"] == split
+    if split == "band":
+        assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] > 0
 
 
 @pytest.mark.parametrize("grid_type", [0, 1, 2])

@@ -516,7 +516,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, work, h_macro, h_E, h_mat, bytes;
+  size_t counts, cursor, btot, mstart, Es, idx, us, work, Et, idxt, h_macro, h_E, h_mat, bytes;
 };
 struct BatchLayout {
   SlotLayout slot;
@@ -559,14 +559,19 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
   };
   const int ch = g->p.bench == GF_XSBENCH ? 5 : 4;
   if (flags & GF_SORT_LOCALITY) {
-    L.counts = take(sizeof(uint32_t) * kBins);
-    L.cursor = take(sizeof(uint32_t) * kBins);
-    L.btot = take(sizeof(uint32_t) * (kBins / kScanBlk));
+    const size_t hw = sort_hist_words(m);
+    L.counts = take(sizeof(uint32_t) * hw);
+    L.cursor = take(sizeof(uint32_t) * hw);
+    L.btot = take(sizeof(uint32_t) * (hw / kScanBlk + 1));
     L.mstart = take(sizeof(uint32_t) * 16);
     L.Es = take(sizeof(double) * m);
     L.idx = take(sizeof(uint32_t) * m);
     L.us = take(sizeof(uint32_t) * m);
     L.work = take(256);
+    if (g->p.bench == GF_XSBENCH && g->p.n_bands > 1) {  // band grids: the compacted in-band lookups (sort.cu)
+      L.Et = take(sizeof(uint64_t) * m);
+      L.idxt = take(sizeof(uint32_t) * m);
+    }
   }
   if (host_io) {
     if (want_macro) L.h_macro = take(sizeof(double) * ch * m);
@@ -605,6 +610,8 @@ static SortScratch slot_sort(char *base, const SlotLayout &L) {
   S.idx = reinterpret_cast<uint32_t *>(base + L.idx);
   S.us = reinterpret_cast<uint32_t *>(base + L.us);
   S.work = reinterpret_cast<uint32_t *>(base + L.work);
+  S.Et = L.Et ? reinterpret_cast<double *>(base + L.Et) : nullptr;
+  S.idxt = L.idxt ? reinterpret_cast<uint32_t *>(base + L.idxt) : nullptr;
   return S;
 }
 

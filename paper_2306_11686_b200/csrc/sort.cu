@@ -1,15 +1,21 @@
 // sort.cu -- A1/A2: sampling and the locality sort on sm_100a.
 //
 // Lookups are ordered by the key (material, floor(E 2^b)) -- b = 17 at 17 M: 12 x 2^17 bins, ~18-36
-// lookups per bin (smaller batches: fewer bins, sort_bits) -- so that neighbouring lookups share intervals in the lookup kernels; order inside a
-// bin is arbitrary (results are order-independent: integer hash, outputs scattered back through idx).
-// Counting sort: sort_count (sample, one global atomic per lookup on its bin), a two-kernel scan,
+// lookups per bin (smaller batches: fewer bins, sort_bits) -- so that neighbouring lookups share
+// intervals in the lookup kernels; order inside a bin is arbitrary (results are order-independent:
+// integer hash, outputs scattered back through idx).
+// Counting sort: sort_count (sample, one global atomic per lookup on its bin), a two-kernel scan (which
+// also writes the material starts and, for unionized tile batches, the per-tile union indices),
 // sort_scatter (sample again, atomic cursor, store E and the lookup position).  Sampling is
-// index-addressed (lookup i draws from fast_forward(seed, 2i)): a thread skips once and steps
-// through kRun consecutive lookups; the material roll is decided on the integer LCG state
-// (pick_material_state, exact).  A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi
-// (the defaults keep all).  Measured alternative: a two-level sort (coarse
-// buckets per CTA run, then a per-bucket fine sort) moved fewer DRAM bytes but was not faster.
+// index-addressed (lookup i draws from fast_forward(seed, 2i)): a thread skips once and steps through
+// 16 consecutive lookups as two interleaved LCG chains; the material roll is decided on the integer LCG
+// state (pick_material_tab, exact).
+// A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi: its count pass (sort_count_band)
+// samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list, and the scatter
+// (sort_scatter_band) reads that list instead of re-sampling.
+// Measured alternatives: a two-level sort (coarse buckets per CTA run, then a
+// per-bucket fine sort), and a two-pass MSD radix sort without global atomics (per-CTA bucket histograms,
+// shared-memory ranks, one CTA per bucket): both moved fewer atomics but were not faster at 17 M.
 #include "gf_internal.cuh"
 
 #include <cstdlib>
@@ -18,10 +24,9 @@
 
 namespace gf {
 
-constexpr int kRun = 16;   // sort_scatter: lookups per thread (registers hold them between phases)
-constexpr int kRunC = 16;  // sort_count: lookups per thread (64 measured: no faster at 17 M, slower for small batches)
+constexpr int kRun = 16;  // lookups per sampling thread (registers hold them between phases)
 constexpr int kSampTpb = 256;
-static_assert(kRun == 16 && kRunC == 16 && kSampTpb == 256, "the offset maps (kOffMapOff) are for 256 x 16 lookups");
+static_assert(kRun == 16 && kSampTpb == 256, "the offset maps (kOffMapOff) are for 256 x 16 lookups");
 
 // A sampling CTA (kSampTpb threads x 16 consecutive lookups): the integer thresholds and the material
 // bucket table go to shared memory; thread 0 skips to the CTA's first lookup once (gen: sampled, not
@@ -46,60 +51,67 @@ __device__ __forceinline__ uint64_t thread_start(const double *thr, const Sample
   return (m.x * Q.base + m.y) & kLcgMask;
 }
 
-// Band filter of a NEXT-2 band grid: [lo, hi).  The defaults (-inf, +inf) mean "no band" and keep
-// every lookup, +-inf and NaN energies included.
 // Sort bins within a material: 2^nbl bins, bin = floor((E - b0) 2^sl) clamped (a whole grid: b0 = 0,
 // sl = nbl, exact scaling).  A band grid's batch covers only its band [b0, b0 + 1/W): its bins span the
 // band at the whole grid's density (sl = nbl + floor(log2 W)), so the zeroing and the scans shrink W-fold.
 // Sampled lookups are filtered on the LCG state instead: E = RN(s) 2^-63 is non-decreasing in s, so
 // band_lo <= E < band_hi exactly when slo <= s < shi (state_threshold), and a lookup outside the band
-// costs its two LCG steps and two compares only.
+// costs its LCG step and one compare.
 struct SortBins {
   double b0;
   int sl, nbl;
-  unsigned long long slo, shi;  // the band on the LCG state (whole grid: 0, 2^63)
+  unsigned long long slo, shi;          // the band on the LCG state (whole grid: 0, 2^63)
+  unsigned long long a2, c2, a16, c16;  // affine maps of 2 and 16 LCG steps (one / eight lookups)
 };
 __device__ __forceinline__ int sort_bin(double E, const SortBins &B) {
   int b = (int)__dmul_rn(__dsub_rn(E, B.b0), (double)(1 << B.sl));
   b = b < 0 ? 0 : b;
   return b > (1 << B.nbl) - 1 ? (1 << B.nbl) - 1 : b;
 }
+__device__ __forceinline__ uint32_t bin_of(double E, int mat, const SortBins &B) {
+  return (uint32_t)((mat << B.nbl) + sort_bin(E, B));
+}
 
-__device__ __forceinline__ bool in_band(double E, double lo, double hi) {
-  const bool whole = lo == -__longlong_as_double(0x7ff0000000000000ll) && hi == __longlong_as_double(0x7ff0000000000000ll);
-  return whole || (E >= lo && E < hi);
-}  // consecutive lookups per thread in the sampling kernels
+// The thread's 16 lookups t0 + r as two interleaved chains of energy states (r and r + 8; the second
+// started through the 16-step map, both stepped by the 2-step map): f(r, s1) with the energy state s1 of
+// lookup t0 + r (its material state is lcg_next(s1)).
+template <typename F>
+__device__ __forceinline__ void sample_run(uint64_t s, const SortBins &B, F &&f) {
+  uint64_t sa = lcg_next(s);
+  uint64_t sb = (B.a16 * sa + B.c16) & kLcgMask;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    f(r, sa);
+    f(r + 8, sb);
+    sa = (B.a2 * sa + B.c2) & kLcgMask;
+    sb = (B.a2 * sb + B.c2) & kLcgMask;
+  }
+}
+
 __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t n, uint64_t seed,
                                                   const double *__restrict__ src_E,
                                                   const uint8_t *__restrict__ src_mat,
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
-                                                  double band_lo, double band_hi, SortBins B,
-                                                  unsigned long long *__restrict__ flag) {
+                                                  SortBins B, unsigned long long *__restrict__ flag) {
   __shared__ SampleSmem Q;
   stage_sampler(Q, thr, first, seed, !src_E);
-  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRunC;
+  const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
-  uint64_t s = 0;
-  if (!src_E) s = thread_start(thr, Q);
-  for (int r = 0; r < kRunC; r++) {
-    uint64_t t = t0 + r;
+  if (!src_E) {
+    sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
+      if (t0 + r < n)
+        atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
+    });
+    return;
+  }
+  for (int r = 0; r < kRun; r++) {
+    const uint64_t t = t0 + r;
     if (t >= n) break;
-    double E;
-    int mat;
-    if (src_E) {
-      E = src_E[t];
-      mat = src_mat[t];
-      if (mat >= kMats || !isfinite(E)) invalid_input(flag);  // outside the input domain: flagged
-      mat = mat < kMats ? mat : kMats - 1;
-      if (!in_band(E, band_lo, band_hi)) continue;
-    } else {
-      const uint64_t s1 = lcg_next(s);
-      s = lcg_next(s1);
-      if (s1 < B.slo || s1 >= B.shi) continue;  // outside the band
-      E = lcg_unit(s1);
-      mat = pick_material_tab(s, Q.tab, Q.sT);  // == pick_material(RN(s) 2^-63, T), exact
-    }
-    atomicAdd(counts + (mat << B.nbl) + sort_bin(E, B), 1u);
+    const double E = src_E[t];
+    int mat = src_mat[t];
+    if (mat >= kMats || !isfinite(E)) invalid_input(flag);  // outside the input domain: flagged
+    mat = mat < kMats ? mat : kMats - 1;
+    atomicAdd(counts + bin_of(E, mat, B), 1u);
   }
 }
 
@@ -132,10 +144,29 @@ __global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restric
   if (tid == kScanBlk - 1) btot[blockIdx.x] = wsum[31];
 }
 
-// Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n).
+// Per-tile union indices (TixSpec, gf_internal.cuh) for sampled batches: bin k of a material holds
+// sorted positions [start, start + count); a full tile t (positions 128 t .. 128 t + 127) takes the lower
+// edge of the bin holding 128 t and the upper edge of the bin holding 128 t + 127.  Bin edges are
+// b0 + k 2^-sl: the lookups of bin k satisfy edge(k) <= E < edge(k + 1) (E - b0 is exact: b0 = 0, or
+// Sterbenz for a band's E in [b0, 2 b0]), and RN is monotone, so RN(edge) bounds E on the same side (bin 0
+// of a material: u = 0).  The batch's last, partial tile is left to the lookup kernel.
+__device__ __forceinline__ void tile_bounds(const TixSpec &T, const SortBins &B, uint32_t lb, uint32_t start,
+                                            uint32_t count) {
+  const uint32_t end = start + count;
+  const double w = exp2(-(double)B.sl);
+  for (uint32_t p = (start + 127u) & ~127u; p < end; p += 128u)
+    T.tix[p >> 7].x = lb == 0u ? 0u : (uint32_t)union_search(T.ubin, T.U, T.n_union, __dadd_rn(B.b0, __dmul_rn((double)lb, w)));
+  for (uint32_t p = start | 127u; p < end; p += 128u)
+    T.tix[p >> 7].y = (uint32_t)union_search(T.ubin, T.U, T.n_union, __dadd_rn(B.b0, __dmul_rn((double)(lb + 1u), w)));
+}
+
+// Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n) and,
+// for sampled unionized tile batches, the per-tile union indices (T.tix).
 __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ cursor, const uint32_t *__restrict__ btot,
-                                                     uint32_t *__restrict__ mstart, int nb_log2) {
+                                                     uint32_t *__restrict__ mstart, const uint32_t *__restrict__ counts,
+                                                     SortBins B, TixSpec T) {
   __shared__ uint32_t s_off;
+  const int nb_log2 = B.nbl;
   const int nblocks = (kMats << nb_log2) / kScanBlk;
   if (threadIdx.x < 32) {
     uint32_t acc = 0;
@@ -154,53 +185,155 @@ __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ curs
   const uint32_t v = cursor[b] + s_off;
   cursor[b] = v;
   if ((b & ((1 << nb_log2) - 1)) == 0) mstart[b >> nb_log2] = v;
+  if (T.tix) {
+    const uint32_t c = counts[b];
+    if (c) tile_bounds(T, B, (uint32_t)b & ((1u << nb_log2) - 1u), v, c);
+  }
 }
 
 __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_t n, uint64_t seed,
                                                     const double *__restrict__ src_E,
                                                     const uint8_t *__restrict__ src_mat,
                                                     const double *__restrict__ thr, uint32_t *__restrict__ cursor,
-                                                    double *__restrict__ Es, uint32_t *__restrict__ idx,
-                                                    double band_lo, double band_hi, SortBins B) {
+                                                    double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B) {
   __shared__ SampleSmem Q;
   stage_sampler(Q, thr, first, seed, !src_E);
-  uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
+  const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
   const int cnt = (int)min((uint64_t)kRun, n - t0);
-  uint64_t s = 0;
-  if (!src_E) s = thread_start(thr, Q);
   // three phases so that the kRun cursor atomics (each an L2 round trip) are in flight together
   double E[kRun];
   uint32_t pos[kRun];
+  if (src_E) {
 #pragma unroll
-  for (int r = 0; r < kRun; r++) {
-    if (r < cnt) {
-      const uint64_t t = t0 + r;
-      pos[r] = 0xFFFFFFFFu;  // (outside the band: dropped)
-      if (src_E) {
-        E[r] = src_E[t];
-        int mat = src_mat[t];
-        mat = mat < kMats ? mat : kMats - 1;
-        if (in_band(E[r], band_lo, band_hi)) pos[r] = (uint32_t)((mat << B.nbl) + sort_bin(E[r], B));
-      } else {
-        const uint64_t s1 = lcg_next(s);
-        s = lcg_next(s1);
-        if (s1 >= B.slo && s1 < B.shi) {
-          E[r] = lcg_unit(s1);
-          const int mat = pick_material_tab(s, Q.tab, Q.sT);  // == pick_material(RN(s) 2^-63, T), exact
-          pos[r] = (uint32_t)((mat << B.nbl) + sort_bin(E[r], B));
-        }
+    for (int r = 0; r < kRun; r++) {
+      pos[r] = 0xFFFFFFFFu;  // (beyond the batch: none)
+      if (r < cnt) {
+        E[r] = src_E[t0 + r];
+        const int mat = src_mat[t0 + r];
+        pos[r] = bin_of(E[r], mat < kMats ? mat : kMats - 1, B);
       }
     }
+  } else {
+    sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
+      E[r] = lcg_unit(s1);
+      pos[r] = r < cnt ? bin_of(E[r], pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B) : 0xFFFFFFFFu;
+    });
   }
 #pragma unroll
   for (int r = 0; r < kRun; r++)
-    if (r < cnt && pos[r] != 0xFFFFFFFFu) pos[r] = atomicAdd(cursor + pos[r], 1u);
+    if (pos[r] != 0xFFFFFFFFu) pos[r] = atomicAdd(cursor + pos[r], 1u);
 #pragma unroll
   for (int r = 0; r < kRun; r++) {
-    if (r < cnt && pos[r] != 0xFFFFFFFFu) {
+    if (pos[r] != 0xFFFFFFFFu) {
       Es[pos[r]] = E[r];
       if (idx) idx[pos[r]] = (uint32_t)(t0 + r);
+    }
+  }
+}
+
+// Band grids, count pass: every thread samples its 16 lookups and queues the in-band energy states in its
+// own shared-memory row (no divergent work per step); then each warp processes its queued lookups 32 at
+// a time with every lane active -- bin count (global atomic) and a slot in the compact list, whose
+// slice the CTA takes with one atomic.  Order in the list is arbitrary (the order inside a bin is anyway).
+constexpr int kQStride = kRun + 1;  // (row stride in u64: lanes' rows in different banks)
+struct BandSmem {
+  unsigned long long q[kSampTpb * kQStride];
+  uint8_t qp[kSampTpb * kRun];
+  uint32_t wpre[kSampTpb / 32][32];
+  uint32_t wtot[kSampTpb / 32];
+  uint32_t base;
+};
+__global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint32_t n, uint64_t seed,
+                                                       const double *__restrict__ thr, uint32_t *__restrict__ counts,
+                                                       SortBins B, uint64_t *__restrict__ cs,
+                                                       uint32_t *__restrict__ cidx, uint32_t *__restrict__ ccount) {
+  __shared__ SampleSmem Q;
+  __shared__ BandSmem M;
+  stage_sampler(Q, thr, first, seed, true);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kSampTpb * kRun;
+  const uint64_t t0 = c0 + (uint64_t)threadIdx.x * kRun;
+  const unsigned long long span = B.shi - B.slo;
+  uint32_t cnt = 0;
+  unsigned long long *row = M.q + threadIdx.x * kQStride;
+  uint8_t *prow = M.qp + threadIdx.x * kRun;
+  if (t0 < n) {
+    sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
+      if (t0 + r < n && s1 - B.slo < span) {
+        row[cnt] = s1;
+        prow[cnt] = (uint8_t)r;
+        cnt++;
+      }
+    });
+  }
+  uint32_t x = cnt;  // warp prefix of the queue lengths
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  M.wpre[w][lane] = x - cnt;
+  if (lane == 31) M.wtot[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int k = 0; k < kSampTpb / 32; k++) {
+      const uint32_t v = M.wtot[k];
+      M.wtot[k] = tot;
+      tot += v;
+    }
+    M.base = tot ? atomicAdd(ccount, tot) : 0u;
+  }
+  __syncthreads();
+  const uint32_t wn = __shfl_sync(0xffffffffu, x, 31), wb = M.base + M.wtot[w];
+  for (uint32_t j = lane; j < wn; j += 32) {
+    int o = 0;  // the lane whose queue holds entry j: max{o : wpre[o] <= j}
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (M.wpre[w][o + step] <= j) o += step;
+    const uint32_t k = j - M.wpre[w][o];
+    const int src = w * 32 + o;
+    const uint64_t s1 = M.q[src * kQStride + k];
+    atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
+    cs[wb + j] = s1;
+    if (cidx) cidx[wb + j] = (uint32_t)(c0 + (uint64_t)src * kRun + M.qp[src * kRun + k]);
+  }
+}
+
+// Band grids, scatter: the compact list's lookups to their sorted positions (a persistent grid, kScatB
+// list entries per thread and round so that their cursor atomics are in flight together).
+constexpr int kScatB = 8;
+__global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restrict__ cs,
+                                                         const uint32_t *__restrict__ cidx,
+                                                         const double *__restrict__ thr, uint32_t *__restrict__ cursor,
+                                                         double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B,
+                                                         const uint32_t *__restrict__ mstart) {
+  __shared__ SampleSmem Q;
+  stage_sampler(Q, thr, 0, 0, false);
+  const uint32_t total = __ldg(mstart + kMats);  // == the compact list's length
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += kScatB * stride) {
+    uint32_t pos[kScatB];
+    uint64_t sv[kScatB];
+#pragma unroll
+    for (int b = 0; b < kScatB; b++) {
+      const uint32_t i = i0 + b * stride;
+      if (i < total) {
+        sv[b] = __ldg(cs + i);
+        pos[b] = bin_of(lcg_unit(sv[b]), pick_material_tab(lcg_next(sv[b]), Q.tab, Q.sT), B);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kScatB; b++)
+      if (i0 + b * stride < total) pos[b] = atomicAdd(cursor + pos[b], 1u);
+#pragma unroll
+    for (int b = 0; b < kScatB; b++) {
+      const uint32_t i = i0 + b * stride;
+      if (i < total) {
+        Es[pos[b]] = lcg_unit(sv[b]);
+        if (idx) idx[pos[b]] = __ldg(cidx + i);
+      }
     }
   }
 }
@@ -228,8 +361,6 @@ static int sort_bits(uint32_t n) {
   return b;
 }
 
-// The bins of an n-lookup batch on a grid with band [lo, hi) ((-inf, inf): whole grid; band 0 is open
-// below, the last band above, their lookups still lie in [0, 1/W) / [(W-1)/W, 1)).
 // min{s in [0, 2^63] : RN(s) 2^-63 >= T} (2^63: none), by bisection with the samplers' conversion (the
 // host's int64 -> double conversion rounds to nearest like __ull2double_rn; the scaling is exact).
 static unsigned long long state_threshold(double T) {
@@ -241,8 +372,20 @@ static unsigned long long state_threshold(double T) {
   return lo;
 }
 
-static SortBins whole_bins(int nb) { return SortBins{0.0, nb, nb, 0ull, 1ull << 63}; }
+static SortBins with_maps(SortBins B) {
+  uint64_t A, C;
+  lcg_skip_map(2, A, C);
+  B.a2 = A;
+  B.c2 = C;
+  lcg_skip_map(16, A, C);
+  B.a16 = A;
+  B.c16 = C;
+  return B;
+}
+static SortBins whole_bins(int nb) { return with_maps(SortBins{0.0, nb, nb, 0ull, 1ull << 63}); }
 
+// The bins of an n-lookup batch on a grid with band [lo, hi) ((-inf, inf): whole grid; band 0 is open
+// below, the last band above, their lookups still lie in [0, 1/W) / [(W-1)/W, 1)).
 static SortBins sort_bins(uint32_t n, double lo, double hi) {
   const int nb = sort_bits(n);
   const bool flo = std::isfinite(lo), fhi = std::isfinite(hi);
@@ -252,45 +395,62 @@ static SortBins sort_bins(uint32_t n, double lo, double hi) {
   int wl = 0;  // floor(log2 W)
   while (wl < 20 && (2l << wl) <= W) wl++;
   const int nbl = nb - wl < 10 ? 10 : nb - wl;
-  return SortBins{flo ? lo : 0.0, nbl + wl, nbl, flo ? state_threshold(lo) : 0ull,
-                  fhi ? state_threshold(hi) : 1ull << 63};
+  return with_maps(SortBins{flo ? lo : 0.0, nbl + wl, nbl, flo ? state_threshold(lo) : 0ull,
+                            fhi ? state_threshold(hi) : 1ull << 63});
 }
 
+// Words of the count / cursor arrays (12 x 2^17 bins, + the compact-list counter of band grids).
+size_t sort_hist_words(uint64_t) { return ((size_t)kMats << 17) + 1; }
+
 cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) {
-  return cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * (kMats << sort_bits(n)), st);
+  return cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * ((size_t)kMats << sort_bits(n)), st);
 }
 
 // Counts caller lookups [0, cn) of a chunk (src_E / src_mat point at the chunk) into the bins of an
 // n_total-lookup batch (no band grids: the host-IO path rejects them).
 cudaError_t launch_sort_count(uint32_t n_total, uint32_t cn, const double *src_E, const uint8_t *src_mat,
                               const double *thr, const SortScratch &S, unsigned long long *flag, cudaStream_t st) {
-  const double inf = HUGE_VAL;
-  const unsigned gc = nblk(((long long)cn + kRunC - 1) / kRunC, kSampTpb);
-  const int nb = sort_bits(n_total);
-  sort_count<<<gc, kSampTpb, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, -inf, inf, whole_bins(nb), flag);
+  const unsigned gc = nblk(((long long)cn + kRun - 1) / kRun, kSampTpb);
+  sort_count<<<gc, kSampTpb, 0, st>>>(0, cn, 0, src_E, src_mat, thr, S.counts, whole_bins(sort_bits(n_total)), flag);
   return cudaGetLastError();
 }
 
 cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, const double *src_E,
                                  const uint8_t *src_mat, const double *thr, const SortScratch &S, bool want_idx,
-                                 unsigned long long *flag, cudaStream_t st, double band_lo, double band_hi) {
+                                 unsigned long long *flag, cudaStream_t st, double band_lo, double band_hi,
+                                 const TixSpec *tix) {
   cudaError_t e;
   const SortBins B = S.counted ? whole_bins(sort_bits(n)) : sort_bins(n, band_lo, band_hi);
-  const int nbl = B.nbl;
-  const int bins = kMats << nbl;  // a multiple of kScanBlk for nbl >= 10
-  const unsigned g = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
+  const int bins = kMats << B.nbl;  // a multiple of kScanBlk for nbl >= 10
+  const TixSpec T = (tix && !src_E) ? *tix : TixSpec{};  // (bin edges bound sampled energies only)
+  // band grids take sampled lookups only (abi.cu): the compact-list path; its counter sits behind the bins
+  const bool band = B.slo != 0ull || B.shi != (1ull << 63);
+  if (band && (src_E || S.counted)) return cudaErrorInvalidValue;
   if (!S.counted) {
-    if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
-    const unsigned gc = nblk(((long long)n + kRunC - 1) / kRunC, kSampTpb);
-    sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, band_lo, band_hi, B, flag);
+    if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * (bins + (band ? 1 : 0)), st)) != cudaSuccess) return e;
+    const unsigned gc = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
+    if (band)
+      sort_count_band<<<gc, kSampTpb, 0, st>>>(first, n, seed, thr, S.counts, B, reinterpret_cast<uint64_t *>(S.Et),
+                                                want_idx ? S.idxt : nullptr, S.counts + bins);
+    else
+      sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, B, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, nbl);
+  scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, S.counts, B, T);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  sort_scatter<<<g, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr,
-                                band_lo, band_hi, B);
+  if (band) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned gs = std::min(nblk(((long long)n + kScatB - 1) / kScatB, 256), (unsigned)sms * 8u);
+    sort_scatter_band<<<gs, 256, 0, st>>>(reinterpret_cast<const uint64_t *>(S.Et), S.idxt, thr, S.cursor, S.Es,
+                                          want_idx ? S.idx : nullptr, B, S.mstart);
+  } else {
+    sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(
+        first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B);
+  }
   return cudaGetLastError();
 }
 

@@ -36,17 +36,7 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 template <int GT>
 __device__ __forceinline__ long long energy_index(const XsDev &X, double E) {
   if (GT == GF_GRID_UNIONIZED) {
-    // #{U <= E} lies in [ubin[b], ubin[b+1]] for b = floor(E 2^20) (ubin[2^20] = n covers E >= 1).
-    const int b = energy_bin(E);
-    long long lo = __ldg(X.ubin + b), hi = __ldg(X.ubin + b + 1);
-    if (b == kUBins - 1) hi = X.n_union;
-    while (lo < hi) {  // c = lo + #{U[lo..hi) <= E}
-      long long mid = (lo + hi) >> 1;
-      if (__ldg(X.U + mid) <= E) lo = mid + 1; else hi = mid;
-    }
-    long long u = lo - 1;
-    u = u < 0 ? 0 : u;
-    return u > X.n_union - 2 ? X.n_union - 2 : u;
+    return union_search(X.ubin, X.U, X.n_union, E);
   } else if (GT == kGridNB) {
     // bin b = floor(E 2^kNbLog2) of the per-nuclide tables for E in [0, 1); otherwise -1 (the interval
     // then comes from the index grid)
@@ -394,6 +384,10 @@ __global__ void __launch_bounds__(kLookupTpb, GF_SORTED_MINB) xs_lookup_sorted(X
 
 #include "xs_tile.cuh"
 
+#ifndef GF_TILE_PREP
+#define GF_TILE_PREP 0  // A/B: 1 = every unionized tile batch takes tile_prep (exact extremes), no scatter tix
+#endif
+
 // Kernel for the sorted path (XsDev::kern, chosen once at grid init).  Default: the warp-tile kernel
 // for dense batches (n >= tile_min; unionized and hash grids), the group kernel (4 lookups per
 // thread, per-lookup searches) for medium ones and the one-lookup-per-thread kernel below group_min:
@@ -414,27 +408,32 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
   const size_t smem = xs_table_smem(X.total);
   cudaError_t e;
   if (sort) {
-    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), vsum, st, X.band_lo, X.band_hi)) !=
-        cudaSuccess)
+    const int kern = sorted_kernel(X, n);
+    // sampled unionized warp-tile batches with per-tile union indices: the scatter writes them (TixSpec);
+    // caller energies (possibly clamped into a material's last bin) take tile_prep's exact tile extremes
+    const bool tix = GT == GF_GRID_UNIONIZED && kern == kKernTile && n >= X.prep_min && !src_E && !GF_TILE_PREP;
+    const TixSpec T{reinterpret_cast<uint2 *>(S.us), X.ubin, X.U, X.n_union};
+    if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), vsum, st, X.band_lo, X.band_hi,
+                                  tix ? &T : nullptr)) != cudaSuccess)
       return e;
     if (ev_mid && (e = cudaEventRecord(ev_mid, st)) != cudaSuccess) return e;
-    const int kern = sorted_kernel(X, n);
     if (GT != GF_GRID_NUCLIDE && kern == kKernGroup)
       return X.fastdiv ? launch_group<GT, true>(X, n, S, out, vsum, st)
                        : launch_group<GT, false>(X, n, S, out, vsum, st);
     if constexpr (GT != GF_GRID_NUCLIDE) {
       if (kern == kKernTile)
-        return X.fastdiv ? launch_tile<GT, true>(X, n, S, out, vsum, st) : launch_tile<GT, false>(X, n, S, out, vsum, st);
+        return X.fastdiv ? launch_tile<GT, true>(X, n, S, out, vsum, st, !tix)
+                         : launch_tile<GT, false>(X, n, S, out, vsum, st, !tix);
     }
     if constexpr (GT == GF_GRID_UNIONIZED) {
       if (kern == kKernTileNB && X.NB)
-        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st)
-                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st);
+        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st, false)
+                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st, false);
     }
     if constexpr (GT == GF_GRID_NUCLIDE) {  // the warp-tile kernel with runs from the NB brackets
       if ((kern == kKernTile || kern == kKernTileNB) && X.XR && X.NB)
-        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st)
-                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st);
+        return X.fastdiv ? launch_tile<kGridNB, true>(X, n, S, out, vsum, st, false)
+                         : launch_tile<kGridNB, false>(X, n, S, out, vsum, st, false);
     }
     if (GT == GF_GRID_NUCLIDE && X.NB && X.nb_on && kern != kKernWarpSearch) {
       if ((e = allow_smem(xs_lookup_sorted<kGridNB>, smem)) != cudaSuccess) return e;

@@ -255,22 +255,37 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
       const uint32_t ra = rb + kRecStride * off;  // shared address of the run's first record
       const uint32_t nbd = cnt - 1u;  // staged boundaries A[klo + 1 .. klo + cnt - 1]
       // lookup 0 by a binary search over the run; the thread's other lookups (a much narrower range)
-      // against the next three boundaries: c_i = ca + [E_i >= bx] + [E_i >= by] while E_i < bz
-      const uint32_t ca = run_count(ra, nbd, eb[0]);
+      // against the next three boundaries: c_i = ca + [E_i >= bx] + [E_i >= by] while E_i < bz.  A run of
+      // one record (nbd = 0, warp-uniform; about half the runs of a dense batch) needs none of it, a run of
+      // two one compare per lookup.
       const long long kInf = 0x7FF0000000000000ll;  // (+inf: no boundary)
-      const long long bx = ca < nbd ? lds64(ra + kRecStride * ca) : kInf;
-      const long long by = ca + 1u < nbd ? lds64(ra + kRecStride * (ca + 1u)) : kInf;
-      const long long bz = ca + 2u < nbd ? lds64(ra + kRecStride * (ca + 2u)) : kInf;
-      const uint32_t cd = ca + (eb[kL - 1] >= bx ? 1u : 0u) + (eb[kL - 1] >= by ? 1u : 0u);
+      uint32_t ca = 0u, cd = 0u;
+      long long bx = kInf, by = kInf;
+      bool slow = false, strad = false;
+      if (nbd == 1u) {  // two records, one boundary (the next most common run): c_i = [E_i >= b1]
+        const long long b1 = lds64(ra);  // (boundary m is the first double of staged record m)
+        ca = eb[0] >= b1 ? 1u : 0u;
+        cd = eb[kL - 1] >= b1 ? 1u : 0u;
+        bx = ca ? kInf : b1;
+        strad = __any_sync(0xffffffffu, ca != cd);
+      } else if (nbd != 0u) {
+        ca = run_count(ra, nbd, eb[0]);
+        bx = ca < nbd ? lds64(ra + kRecStride * ca) : kInf;
+        by = ca + 1u < nbd ? lds64(ra + kRecStride * (ca + 1u)) : kInf;
+        const long long bz = ca + 2u < nbd ? lds64(ra + kRecStride * (ca + 2u)) : kInf;
+        cd = ca + (eb[kL - 1] >= bx ? 1u : 0u) + (eb[kL - 1] >= by ? 1u : 0u);
+        // common case: no lookup of the warp beyond a cut run, and no thread's lookups span more than two
+        // boundaries (E_3 < bz)
+        slow = __any_sync(0xffffffffu, (wide && cd == nbd) || eb[kL - 1] >= bz);
+        strad = __any_sync(0xffffffffu, ca != cd);
+      }
       const double conc = tab_conc(T, jj, true);
       Rec P;
-      // common case: no lookup of the warp beyond a cut run, and no thread's lookups span more than two
-      // boundaries (E_3 < bz)
-      if (!__any_sync(0xffffffffu, (wide && cd == nbd) || eb[kL - 1] >= bz)) {
+      if (!slow) {
         const uint32_t sa = ra;
         uint32_t cP = ca;
         lds_rec<FAST>(ra + kRecStride * ca, P);
-        if (!__any_sync(0xffffffffu, ca != cd)) {  // no thread straddles: the 4 chains interleave
+        if (!strad) {  // no thread straddles: the 4 chains interleave
 #pragma unroll
           for (int i = 0; i < kL; i++) accumulate_rec<FAST>(P, E[i], conc, m[i]);
         } else {
@@ -548,12 +563,14 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
           for (int c = 0; c < 5; c++) m[i][c] = 0.0;
         double Emin, Emax;
         uint32_t imin, imax;
-        if (GT == GF_GRID_UNIONIZED && PREP && mat0 == mat1) {  // one pass: the tile's range, its indices from tile_prep
+        if (GT == GF_GRID_UNIONIZED && PREP && mat0 == mat1 && P + 32 * kL <= n) {  // a full tile in one material:
+          // the tile's range, its union indices from the sort (sampled batches) or tile_prep
           Emin = __longlong_as_double(tlo);
           Emax = __longlong_as_double(thi);
           imin = tu.x;
           imax = tu.y;
-        } else if (GT == GF_GRID_UNIONIZED && PREP) {  // a pass of a tile across a material boundary: its own range
+        } else if (GT == GF_GRID_UNIONIZED && PREP) {  // a pass of a tile across a material boundary (or the
+          // batch's last, partial tile): its own range
           Emin = __longlong_as_double(warp_min64(__double_as_longlong(E[0])));
           Emax = __longlong_as_double(warp_max64(__double_as_longlong(E[kL - 1])));
           const uint2 u = union_range(X, Emin, Emax);
@@ -631,7 +648,7 @@ __global__ void __launch_bounds__(256) tile_prep(XsDev X, uint32_t n, const doub
 
 template <int GT, bool FAST, bool PREP>
 static cudaError_t launch_tile_p(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
-                               unsigned long long *vsum, cudaStream_t st) {
+                               unsigned long long *vsum, cudaStream_t st, bool tile_prep_on) {
   const size_t smem = tile_smem(X.total);
   int blocks_per_sm = 0;
   cudaError_t e;
@@ -647,9 +664,13 @@ static cudaError_t launch_tile_p(const XsDev &X, uint32_t n, const SortScratch &
   const uint32_t ntiles = (n + 32 * kL - 1) / (32 * kL);
   const uint32_t grid =
       max(1u, min((ntiles + kTileWarps - 1) / kTileWarps, (uint32_t)(sms * max(blocks_per_sm, 1))));
-  if (GT == GF_GRID_UNIONIZED && PREP) {  // per-tile union indices (S.us holds uint2 per tile)
-    tile_prep<<<nblk((long long)ntiles * 32, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, reinterpret_cast<uint2 *>(S.us));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (GT == GF_GRID_UNIONIZED && PREP) {
+    // per-tile union indices (S.us holds uint2 per tile): written by the sort's scatter for sampled
+    // batches (TixSpec, launch_gt), else by tile_prep (the exact tile extremes, one warp per tile)
+    if (tile_prep_on) {
+      tile_prep<<<nblk((long long)ntiles * 32, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, reinterpret_cast<uint2 *>(S.us));
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
   } else if (GT != kGridNB) {  // per-lookup hash bins (the bin-interior check)
     idx_prep<GT><<<nblk(((long long)n + 3) / 4, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -661,9 +682,9 @@ static cudaError_t launch_tile_p(const XsDev &X, uint32_t n, const SortScratch &
 
 template <int GT, bool FAST>
 static cudaError_t launch_tile(const XsDev &X, uint32_t n, const SortScratch &S, const OutSpec &out,
-                               unsigned long long *vsum, cudaStream_t st) {
+                               unsigned long long *vsum, cudaStream_t st, bool tile_prep_on) {
   if constexpr (GT == GF_GRID_UNIONIZED) {
-    if (n >= X.prep_min) return launch_tile_p<GT, FAST, true>(X, n, S, out, vsum, st);
+    if (n >= X.prep_min) return launch_tile_p<GT, FAST, true>(X, n, S, out, vsum, st, tile_prep_on);
   }
-  return launch_tile_p<GT, FAST, false>(X, n, S, out, vsum, st);
+  return launch_tile_p<GT, FAST, false>(X, n, S, out, vsum, st, false);
 }

@@ -677,6 +677,18 @@ def test_C7_bands_sum_to_xl(gf, torch):
     assert raw == gold["C6"]["raw"]
 
 
+@pytest.mark.parametrize("W,b", [(8, 0), (8, 5), (8, 7), (3, 2)])
+def test_band_tile_path_per_lookup(gf, torch, W, b):
+    """A C3 band replica through the warp-tile kernel with the per-tile union indices the sort's scatter
+    writes (sort-bin edges, TixSpec) and the compacted in-band list of the band sort: every in-band row
+    equals the oracle's bitwise (its nuclide grid gives identical intervals), the others stay untouched."""
+    o = O.XSOracle(355, 11303, O.NUCLIDE)
+    g = gf.Grid(gf.Params.xsbench(355, 11303, gf.UNIONIZED, n_bands=W, band=b))
+    g.set_kernel("tile")
+    g.set_prep_min(0)
+    check_bands_one(gf, torch, o, g, W, b, 5_000_000, 400_000)
+
+
 def check_bands_one(gf, torch, o, g, W, b, first, n):
     raw_o, m_o = o.lookup_batch(first, n, want_macro=True)
     E = np.array([O.sample(first + i)[0] for i in range(n)])

@@ -516,7 +516,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, work, Et, idxt, h_macro, h_E, h_mat, bytes;
+  size_t counts, cursor, btot, mstart, Es, idx, us, work, Et, idxt, rk, h_macro, h_E, h_mat, bytes;
 };
 struct BatchLayout {
   SlotLayout slot;
@@ -571,6 +571,7 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
     if (g->p.bench == GF_XSBENCH && g->p.n_bands > 1) {  // band grids: the compacted in-band lookups (sort.cu)
       L.Et = take(sizeof(uint64_t) * m);
       L.idxt = take(sizeof(uint32_t) * m);
+      L.rk = take(sizeof(uint32_t) * m);
     }
   }
   if (host_io) {
@@ -612,6 +613,7 @@ static SortScratch slot_sort(char *base, const SlotLayout &L) {
   S.work = reinterpret_cast<uint32_t *>(base + L.work);
   S.Et = L.Et ? reinterpret_cast<double *>(base + L.Et) : nullptr;
   S.idxt = L.idxt ? reinterpret_cast<uint32_t *>(base + L.idxt) : nullptr;
+  S.rk = L.rk ? reinterpret_cast<uint32_t *>(base + L.rk) : nullptr;
   return S;
 }
 

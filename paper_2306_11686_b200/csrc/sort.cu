@@ -11,8 +11,9 @@
 // 16 consecutive lookups as two interleaved LCG chains; the material roll is decided on the integer LCG
 // state (pick_material_tab, exact).
 // A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi: its count pass (sort_count_band)
-// samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list, and the scatter
-// (sort_scatter_band) reads that list instead of re-sampling.
+// samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list with each one's rank
+// inside its bin (the count atomic's return value), and the scatter (sort_scatter_band) places that list
+// without re-sampling or atomics.
 // Measured alternatives: a two-level sort (coarse buckets per CTA run, then a
 // per-bucket fine sort), and a two-pass MSD radix sort without global atomics (per-CTA bucket histograms,
 // shared-memory ranks, one CTA per bucket): both moved fewer atomics but were not faster at 17 M.
@@ -29,9 +30,9 @@ constexpr int kSampTpb = 256;
 static_assert(kRun == 16 && kSampTpb == 256, "the offset maps (kOffMapOff) are for 256 x 16 lookups");
 
 // A sampling CTA (kSampTpb threads x 16 consecutive lookups): the integer thresholds and the material
-// bucket table go to shared memory; thread 0 skips to the CTA's first lookup once (gen: sampled, not
-// caller, energies) and every thread starts from it through the offset map of its 32 t steps -- one
-// affine map instead of a ~25-step skip per thread.
+// bucket table go to shared memory; warp 0 skips to the CTA's first lookup once (gen: sampled, not
+// caller, energies; lcg_skip_warp) and every thread starts from it through the offset map of its 32 t
+// steps -- one affine map instead of a ~25-step skip per thread.
 struct SampleSmem {
   unsigned long long sT[kMats];
   unsigned long long base;
@@ -42,7 +43,10 @@ __device__ __forceinline__ void stage_sampler(SampleSmem &Q, const double *thr, 
   const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
   if (threadIdx.x < kMats) Q.sT[threadIdx.x] = reinterpret_cast<const unsigned long long *>(thr)[kMats + threadIdx.x];
   reinterpret_cast<uint4 *>(Q.tab)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(tb + kMatTabOff) + threadIdx.x);
-  if (gen && threadIdx.x == 0) Q.base = lcg_skip(seed, 2ull * (first + (uint64_t)blockIdx.x * kSampTpb * kRun));
+  if (gen && threadIdx.x < 32) {  // (warp 0: the skip as one warp-wide composition, not one thread's chain)
+    const uint64_t b = lcg_skip_warp(seed, 2ull * (first + (uint64_t)blockIdx.x * kSampTpb * kRun));
+    if (threadIdx.x == 0) Q.base = b;
+  }
   __syncthreads();
 }
 __device__ __forceinline__ uint64_t thread_start(const double *thr, const SampleSmem &Q) {
@@ -150,14 +154,27 @@ __global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restric
 // b0 + k 2^-sl: the lookups of bin k satisfy edge(k) <= E < edge(k + 1) (E - b0 is exact: b0 = 0, or
 // Sterbenz for a band's E in [b0, 2 b0]), and RN is monotone, so RN(edge) bounds E on the same side (bin 0
 // of a material: u = 0).  The batch's last, partial tile is left to the lookup kernel.
+// u(e) at a bin edge e: a multiple of 2^-20 (whole grids, power-of-two bands) is a top-level bin edge of
+// the two-level search, so #{U <= e} = ubin[e 2^20] + #{U == e} (two dependent loads); else the search.
+__device__ __forceinline__ uint32_t edge_union(const TixSpec &T, double e) {
+  const double t = __dmul_rn(e, (double)kUBins);  // (exact scaling)
+  if (t >= 0.0 && t <= (double)kUBins && t == floor(t)) {
+    long long k = __ldg(T.ubin + (int)t);
+    while (k < T.n_union && __ldg(T.U + k) == e) k++;
+    long long u = k - 1;
+    u = u < 0 ? 0 : u;
+    return (uint32_t)(u > T.n_union - 2 ? T.n_union - 2 : u);
+  }
+  return (uint32_t)union_search(T.ubin, T.U, T.n_union, e);
+}
 __device__ __forceinline__ void tile_bounds(const TixSpec &T, const SortBins &B, uint32_t lb, uint32_t start,
                                             uint32_t count) {
   const uint32_t end = start + count;
   const double w = exp2(-(double)B.sl);
   for (uint32_t p = (start + 127u) & ~127u; p < end; p += 128u)
-    T.tix[p >> 7].x = lb == 0u ? 0u : (uint32_t)union_search(T.ubin, T.U, T.n_union, __dadd_rn(B.b0, __dmul_rn((double)lb, w)));
+    T.tix[p >> 7].x = lb == 0u ? 0u : edge_union(T, __dadd_rn(B.b0, __dmul_rn((double)lb, w)));
   for (uint32_t p = start | 127u; p < end; p += 128u)
-    T.tix[p >> 7].y = (uint32_t)union_search(T.ubin, T.U, T.n_union, __dadd_rn(B.b0, __dmul_rn((double)(lb + 1u), w)));
+    T.tix[p >> 7].y = edge_union(T, __dadd_rn(B.b0, __dmul_rn((double)(lb + 1u), w)));
 }
 
 // Adds the exclusive prefix of the CTA totals; records material starts mstart[m] (mstart[12] = n) and,
@@ -247,7 +264,8 @@ struct BandSmem {
 __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint32_t n, uint64_t seed,
                                                        const double *__restrict__ thr, uint32_t *__restrict__ counts,
                                                        SortBins B, uint64_t *__restrict__ cs,
-                                                       uint32_t *__restrict__ cidx, uint32_t *__restrict__ ccount) {
+                                                       uint32_t *__restrict__ rk, uint32_t *__restrict__ cidx,
+                                                       uint32_t *__restrict__ ccount) {
   __shared__ SampleSmem Q;
   __shared__ BandSmem M;
   stage_sampler(Q, thr, first, seed, true);
@@ -295,46 +313,30 @@ __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint
     const uint32_t k = j - M.wpre[w][o];
     const int src = w * 32 + o;
     const uint64_t s1 = M.q[src * kQStride + k];
-    atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
+    // the rank inside the bin comes back with the count (so the scatter needs no atomics)
+    rk[wb + j] = atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
     cs[wb + j] = s1;
     if (cidx) cidx[wb + j] = (uint32_t)(c0 + (uint64_t)src * kRun + M.qp[src * kRun + k]);
   }
 }
 
-// Band grids, scatter: the compact list's lookups to their sorted positions (a persistent grid, kScatB
-// list entries per thread and round so that their cursor atomics are in flight together).
-constexpr int kScatB = 8;
-__global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restrict__ cs,
+// Band grids, scatter: the compact list's lookups to their sorted positions, bin start + the rank the
+// count pass got (no atomics).
+__global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restrict__ cs, const uint32_t *__restrict__ rk,
                                                          const uint32_t *__restrict__ cidx,
-                                                         const double *__restrict__ thr, uint32_t *__restrict__ cursor,
-                                                         double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B,
+                                                         const double *__restrict__ thr,
+                                                         const uint32_t *__restrict__ cursor, double *__restrict__ Es,
+                                                         uint32_t *__restrict__ idx, SortBins B,
                                                          const uint32_t *__restrict__ mstart) {
   __shared__ SampleSmem Q;
   stage_sampler(Q, thr, 0, 0, false);
   const uint32_t total = __ldg(mstart + kMats);  // == the compact list's length
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += kScatB * stride) {
-    uint32_t pos[kScatB];
-    uint64_t sv[kScatB];
-#pragma unroll
-    for (int b = 0; b < kScatB; b++) {
-      const uint32_t i = i0 + b * stride;
-      if (i < total) {
-        sv[b] = __ldg(cs + i);
-        pos[b] = bin_of(lcg_unit(sv[b]), pick_material_tab(lcg_next(sv[b]), Q.tab, Q.sT), B);
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < kScatB; b++)
-      if (i0 + b * stride < total) pos[b] = atomicAdd(cursor + pos[b], 1u);
-#pragma unroll
-    for (int b = 0; b < kScatB; b++) {
-      const uint32_t i = i0 + b * stride;
-      if (i < total) {
-        Es[pos[b]] = lcg_unit(sv[b]);
-        if (idx) idx[pos[b]] = __ldg(cidx + i);
-      }
-    }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint64_t s1 = __ldg(cs + i);
+    const double E = lcg_unit(s1);
+    const uint32_t p = __ldg(cursor + bin_of(E, pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B)) + __ldg(rk + i);
+    Es[p] = E;
+    if (idx) idx[p] = __ldg(cidx + i);
   }
 }
 
@@ -431,7 +433,7 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
     const unsigned gc = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
     if (band)
       sort_count_band<<<gc, kSampTpb, 0, st>>>(first, n, seed, thr, S.counts, B, reinterpret_cast<uint64_t *>(S.Et),
-                                                want_idx ? S.idxt : nullptr, S.counts + bins);
+                                                S.rk, want_idx ? S.idxt : nullptr, S.counts + bins);
     else
       sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, B, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -444,8 +446,8 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned gs = std::min(nblk(((long long)n + kScatB - 1) / kScatB, 256), (unsigned)sms * 8u);
-    sort_scatter_band<<<gs, 256, 0, st>>>(reinterpret_cast<const uint64_t *>(S.Et), S.idxt, thr, S.cursor, S.Es,
+    const unsigned gs = std::min(nblk(n, 256), (unsigned)sms * 8u);
+    sort_scatter_band<<<gs, 256, 0, st>>>(reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, thr, S.cursor, S.Es,
                                           want_idx ? S.idx : nullptr, B, S.mstart);
   } else {
     sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(

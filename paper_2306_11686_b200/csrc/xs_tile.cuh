@@ -104,6 +104,16 @@ __device__ __forceinline__ long long lds64(uint32_t a) {
   asm("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint2 lds_u2(uint32_t a) {
   uint2 v;
   asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
@@ -223,6 +233,7 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
   long long eb[kL];
 #pragma unroll
   for (int i = 0; i < kL; i++) eb[i] = __double_as_longlong(E[i]);
+  const uint32_t csa = smem_u32(T.pk) + 8u;  // concentration of table entry j: csa + 16 j (PK layout)
   __syncwarp();  // the previous tile's readers of S are done
   // prologue: stage chunks 0 and 1, search the candidates after them
   int cs0 = j0, cn0, cs1, cn1 = 0, nxt;
@@ -246,12 +257,15 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
       asm volatile("cp.async.wait_group 0;\n mov.u32 %0, 0;" : "=r"(tok) :: "memory");
     __syncwarp();
     const uint32_t mb = smem_u32(&S.meta[b][0]) + tok, rb = smem_u32(&S.rec[b][0][0]) + tok;
+    // the concentration by a 32-bit shared address (through the generic table pointer ptxas re-derived
+    // the shared window, S2UR + ULEA, in every iteration)
 #pragma unroll kTileUnroll
     for (int s = 0; s < cn0; s++) {
       const int jj = cs0 + s;
-      const uint2 mt = lds_u2(mb + 8u * (uint32_t)s);
-      const uint32_t off = mt.y & 0xFFu, cnt = (mt.y >> 8) & 0xFFu;
-      const bool wide = (mt.y >> 16) != 0u;
+      const uint32_t my = lds_u32(mb + 8u * (uint32_t)s + 4u);
+      const double conc = lds_f64(csa + 16u * (uint32_t)jj);
+      const uint32_t off = my & 0xFFu, cnt = (my >> 8) & 0xFFu;
+      const bool wide = (my >> 16) != 0u;
       const uint32_t ra = rb + kRecStride * off;  // shared address of the run's first record
       const uint32_t nbd = cnt - 1u;  // staged boundaries A[klo + 1 .. klo + cnt - 1]
       // lookup 0 by a binary search over the run; the thread's other lookups (a much narrower range)
@@ -279,7 +293,6 @@ __device__ __forceinline__ void tile_loop(const XsDev &X, const XsTables &T, Til
         slow = __any_sync(0xffffffffu, (wide && cd == nbd) || eb[kL - 1] >= bz);
         strad = __any_sync(0xffffffffu, ca != cd);
       }
-      const double conc = tab_conc(T, jj, true);
       Rec P;
       if (!slow) {
         const uint32_t sa = ra;

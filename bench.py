@@ -87,12 +87,16 @@ def oracle_run(o, cfg, first, n, threads):
     return o.lookup_batch(first, n, threads=threads), n
 
 
-def launches_per_step(bench, gt, sorted_, kern=""):
-    """Our kernels per step: sort_count, scan_local, scan_add, sort_scatter (A1-A2), then the lookup
-    kernel; the unionized / hash tile and group kernels are preceded by idx_prep (A3)."""
+def launches_per_step(bench, gt, sorted_, kern="", n=0, slices=1):
+    """Our kernels per step: the sort's count, scan_local, scan_add and `slices` scatter launches (A1-A2;
+    band grids: sort_count_band, the scans, sort_scatter_band), then the lookup kernel.  idx_prep (A3)
+    precedes the hash-grid tile / group kernels and the unionized ones below 8 M lookups; sampled
+    unionized tile batches from 8 M lookups get their per-tile union indices from scan_add."""
     if not sorted_:
         return 1
-    return 4 + (2 if (bench == "xs" and gt in (1, 2) and kern in ("tile", "group", "")) else 1)  # (+ tile_prep / idx_prep)
+    prep = bench == "xs" and ((gt == 2 and kern in ("tile", "group", "")) or
+                              (gt == 1 and (kern == "group" or (kern in ("tile", "") and n < (8 << 20)))))
+    return 3 + slices + 1 + (1 if prep else 0)
 
 
 def load_profile(cfg, sorted_):
@@ -873,7 +877,7 @@ def main():
                      "tilenb": "xs_lookup_tile<nuclide grid> (warp tiles, runs from the per-nuclide bin brackets)"}.get(
                 kern, "xs_lookup_warp_nuclide (warp-cooperative search)")
         else:
-            kname = {"tile": f"xs_lookup_tile<{gname}> (warp tiles, SMEM-staged interval runs; + tile_prep / idx_prep)",
+            kname = {"tile": f"xs_lookup_tile<{gname}> (warp tiles, SMEM-staged interval runs; + idx_prep where used)",
                      "group": f"xs_lookup_group<{gname}> (+ idx_prep)",
                      "thread": "xs_lookup_sorted<kGridNB> (one lookup per thread)"}.get(kern, kern)
         if HL:
@@ -938,7 +942,9 @@ def main():
             "roofline": roof, "rho": rho, "strong_proxy": proxy, "strong_proxy_band": proxy_band,
             "paper_context": paper,
             "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY, kern) if not HL else
+            "gpu_launches": K * (launches_per_step(bench, gt, flags & gf.SORT_LOCALITY, kern, per_launch_lookups,
+                                                   1 if banded else int(os.environ.get("GF_SCATTER_SLICES", "2")))
+                                 if not HL else
                                  (1 if args.hist_mode == "direct" else
                                   HL * (1 + launches_per_step(bench, gt, flags & gf.SORT_LOCALITY)))),
             "clocks": clk,

@@ -249,6 +249,12 @@ static void kernel_choice(XsDev &X) {
   X.tile_min = kTileMinN;
   if (const char *m = getenv("GF_XS_TILE_MIN")) X.tile_min = (uint32_t)strtoul(m, nullptr, 10);
   X.group_min = kGroupMinN;
+  if (X.grid_type == GF_GRID_HASH && X.n_gp > 65536) {
+    // XL hash grids (C6): a tile's runs outgrow the staging buffers for the sparse materials, and the
+    // group kernel wins from 2 M lookups (gpurun_out/r02ak, C6 17 M: group 15.7 ms, tile 17.4, thread 19.9)
+    X.tile_min = 0xFFFFFFFFu;
+    X.group_min = kTileMinN;
+  }
   X.prep_min = 8u << 20;
   if (const char *m = getenv("GF_XS_GROUP_MIN")) X.group_min = (uint32_t)strtoul(m, nullptr, 10);
   const char *nb = getenv("GF_XS_NB");
@@ -516,7 +522,7 @@ gf_status gf_xs_grid_array(const gf_xs_grid *g, int32_t which, const void **ptr,
 constexpr uint64_t kIoChunk = 1ull << GF_IO_CHUNK_LOG2;
 
 struct SlotLayout {
-  size_t counts, cursor, btot, mstart, Es, idx, us, work, Et, idxt, rk, h_macro, h_E, h_mat, bytes;
+  size_t counts, cursor, btot, mstart, Es, idx, us, work, Et, idxt, rk, segcnt, h_macro, h_E, h_mat, bytes;
 };
 struct BatchLayout {
   SlotLayout slot;
@@ -572,6 +578,7 @@ static void plan_slot(const gf_xs_grid *g, uint64_t m, uint32_t flags, bool want
       L.Et = take(sizeof(uint64_t) * m);
       L.idxt = take(sizeof(uint32_t) * m);
       L.rk = take(sizeof(uint32_t) * m);
+      L.segcnt = take(sizeof(uint32_t) * (m / 512 + 1));
     }
   }
   if (host_io) {
@@ -614,6 +621,7 @@ static SortScratch slot_sort(char *base, const SlotLayout &L) {
   S.Et = L.Et ? reinterpret_cast<double *>(base + L.Et) : nullptr;
   S.idxt = L.idxt ? reinterpret_cast<uint32_t *>(base + L.idxt) : nullptr;
   S.rk = L.rk ? reinterpret_cast<uint32_t *>(base + L.rk) : nullptr;
+  S.segcnt = L.segcnt ? reinterpret_cast<uint32_t *>(base + L.segcnt) : nullptr;
   return S;
 }
 

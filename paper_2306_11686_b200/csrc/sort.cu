@@ -11,9 +11,9 @@
 // 16 consecutive lookups as two interleaved LCG chains; the material roll is decided on the integer LCG
 // state (pick_material_tab, exact).
 // A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi: its count pass (sort_count_band)
-// samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list with each one's rank
-// inside its bin (the count atomic's return value), and the scatter (sort_scatter_band) places that list
-// without re-sampling or atomics.
+// samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list (per-warp segments)
+// with each one's rank inside its bin (the count atomic's return value), and the scatter
+// (sort_scatter_band) places that list without re-sampling or atomics.
 // Measured alternatives: a two-level sort (coarse buckets per CTA run, then a
 // per-bucket fine sort), and a two-pass MSD radix sort without global atomics (per-CTA bucket histograms,
 // shared-memory ranks, one CTA per bucket): both moved fewer atomics but were not faster at 17 M.
@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_
                                                     const double *__restrict__ src_E,
                                                     const uint8_t *__restrict__ src_mat,
                                                     const double *__restrict__ thr, uint32_t *__restrict__ cursor,
-                                                    double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B) {
+                                                    double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B,
+                                                    unsigned long long slo, unsigned long long sspan) {
   __shared__ SampleSmem Q;
   stage_sampler(Q, thr, first, seed, !src_E);
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
@@ -234,7 +235,8 @@ __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_
   } else {
     sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
       E[r] = lcg_unit(s1);
-      pos[r] = r < cnt ? bin_of(E[r], pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B) : 0xFFFFFFFFu;
+      pos[r] = (r < cnt && s1 - slo < sspan) ? bin_of(E[r], pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B)
+                                              : 0xFFFFFFFFu;
     });
   }
 #pragma unroll
@@ -249,94 +251,89 @@ __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_
   }
 }
 
-// Band grids, count pass: every thread samples its 16 lookups and queues the in-band energy states in its
-// own shared-memory row (no divergent work per step); then each warp processes its queued lookups 32 at
-// a time with every lane active -- bin count (global atomic) and a slot in the compact list, whose
-// slice the CTA takes with one atomic.  Order in the list is arbitrary (the order inside a bin is anyway).
+// Band grids, count pass, one warp per 512 consecutive lookups (a segment) and no CTA barrier: the warp
+// skips to its segment (lcg_skip_warp), every lane samples its 16 lookups and queues the in-band energy
+// states in its own shared-memory row (no divergent work per step); then the warp processes its queue 32
+// entries at a time with every lane active: one returning atomic per kept lookup (its bin count, and its
+// rank inside the bin for the scatter), the state and rank stored at the segment's slots of the compact
+// list (capacity 512 per segment) and the segment's length in segcnt.
+constexpr int kSeg = 32 * kRun;     // lookups per warp segment
 constexpr int kQStride = kRun + 1;  // (row stride in u64: lanes' rows in different banks)
-struct BandSmem {
-  unsigned long long q[kSampTpb * kQStride];
-  uint8_t qp[kSampTpb * kRun];
-  uint32_t wpre[kSampTpb / 32][32];
-  uint32_t wtot[kSampTpb / 32];
-  uint32_t base;
-};
 __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint32_t n, uint64_t seed,
                                                        const double *__restrict__ thr, uint32_t *__restrict__ counts,
                                                        SortBins B, uint64_t *__restrict__ cs,
                                                        uint32_t *__restrict__ rk, uint32_t *__restrict__ cidx,
-                                                       uint32_t *__restrict__ ccount) {
-  __shared__ SampleSmem Q;
-  __shared__ BandSmem M;
-  stage_sampler(Q, thr, first, seed, true);
+                                                       uint32_t *__restrict__ segcnt) {
+  __shared__ unsigned long long q[kSampTpb * kQStride];
+  __shared__ uint8_t qp[kSampTpb * kRun];
+  __shared__ uint32_t wpre[kSampTpb / 32][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t c0 = (uint64_t)blockIdx.x * kSampTpb * kRun;
-  const uint64_t t0 = c0 + (uint64_t)threadIdx.x * kRun;
+  const uint32_t g = blockIdx.x * (kSampTpb / 32) + w;  // segment
+  const uint64_t w0 = (uint64_t)g * kSeg;
+  if (w0 >= n) return;  // (warp-uniform)
+  const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
+  const uint8_t *tab = tb + kMatTabOff;
+  const unsigned long long *sT = reinterpret_cast<const unsigned long long *>(thr) + kMats;
+  const uint64_t base = lcg_skip_warp(seed, 2ull * (first + w0));
+  const ulonglong2 m = __ldg(reinterpret_cast<const ulonglong2 *>(tb + kOffMapOff) + lane);  // 32 lane steps
+  const uint64_t t0 = w0 + (uint64_t)lane * kRun;
   const unsigned long long span = B.shi - B.slo;
   uint32_t cnt = 0;
-  unsigned long long *row = M.q + threadIdx.x * kQStride;
-  uint8_t *prow = M.qp + threadIdx.x * kRun;
-  if (t0 < n) {
-    sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
-      if (t0 + r < n && s1 - B.slo < span) {
-        row[cnt] = s1;
-        prow[cnt] = (uint8_t)r;
-        cnt++;
-      }
-    });
-  }
+  unsigned long long *row = q + threadIdx.x * kQStride;
+  uint8_t *prow = qp + threadIdx.x * kRun;
+  sample_run((m.x * base + m.y) & kLcgMask, B, [&](int r, uint64_t s1) {
+    if (t0 + r < n && s1 - B.slo < span) {
+      row[cnt] = s1;
+      prow[cnt] = (uint8_t)r;
+      cnt++;
+    }
+  });
   uint32_t x = cnt;  // warp prefix of the queue lengths
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  M.wpre[w][lane] = x - cnt;
-  if (lane == 31) M.wtot[w] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t tot = 0;
-    for (int k = 0; k < kSampTpb / 32; k++) {
-      const uint32_t v = M.wtot[k];
-      M.wtot[k] = tot;
-      tot += v;
-    }
-    M.base = tot ? atomicAdd(ccount, tot) : 0u;
-  }
-  __syncthreads();
-  const uint32_t wn = __shfl_sync(0xffffffffu, x, 31), wb = M.base + M.wtot[w];
+  wpre[w][lane] = x - cnt;
+  const uint32_t wn = __shfl_sync(0xffffffffu, x, 31);
+  if (lane == 0) segcnt[g] = wn;
+  __syncwarp();
   for (uint32_t j = lane; j < wn; j += 32) {
     int o = 0;  // the lane whose queue holds entry j: max{o : wpre[o] <= j}
 #pragma unroll
     for (int step = 16; step > 0; step >>= 1)
-      if (M.wpre[w][o + step] <= j) o += step;
-    const uint32_t k = j - M.wpre[w][o];
+      if (wpre[w][o + step] <= j) o += step;
+    const uint32_t k = j - wpre[w][o];
     const int src = w * 32 + o;
-    const uint64_t s1 = M.q[src * kQStride + k];
-    // the rank inside the bin comes back with the count (so the scatter needs no atomics)
-    rk[wb + j] = atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
-    cs[wb + j] = s1;
-    if (cidx) cidx[wb + j] = (uint32_t)(c0 + (uint64_t)src * kRun + M.qp[src * kRun + k]);
+    const uint64_t s1 = q[src * kQStride + k];
+    const size_t slot = (size_t)w0 + j;
+    rk[slot] = atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), tab, sT), B), 1u);
+    cs[slot] = s1;
+    if (cidx) cidx[slot] = (uint32_t)(w0 + (uint64_t)o * kRun + qp[src * kRun + k]);
   }
 }
 
-// Band grids, scatter: the compact list's lookups to their sorted positions, bin start + the rank the
-// count pass got (no atomics).
+// Band grids, scatter: one warp per segment places its kept lookups at bin start + rank (no atomics).
 __global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restrict__ cs, const uint32_t *__restrict__ rk,
                                                          const uint32_t *__restrict__ cidx,
+                                                         const uint32_t *__restrict__ segcnt, uint32_t nseg,
                                                          const double *__restrict__ thr,
                                                          const uint32_t *__restrict__ cursor, double *__restrict__ Es,
-                                                         uint32_t *__restrict__ idx, SortBins B,
-                                                         const uint32_t *__restrict__ mstart) {
-  __shared__ SampleSmem Q;
-  stage_sampler(Q, thr, 0, 0, false);
-  const uint32_t total = __ldg(mstart + kMats);  // == the compact list's length
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint64_t s1 = __ldg(cs + i);
+                                                         uint32_t *__restrict__ idx, SortBins B) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g >= nseg) return;
+  const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
+  const uint8_t *tab = tb + kMatTabOff;
+  const unsigned long long *sT = reinterpret_cast<const unsigned long long *>(thr) + kMats;
+  const uint32_t c = __ldg(segcnt + g);
+  for (uint32_t j = lane; j < c; j += 32) {
+    const size_t slot = (size_t)g * kSeg + j;
+    const uint64_t s1 = __ldg(cs + slot);
     const double E = lcg_unit(s1);
-    const uint32_t p = __ldg(cursor + bin_of(E, pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B)) + __ldg(rk + i);
+    const uint32_t p = __ldg(cursor + bin_of(E, pick_material_tab(lcg_next(s1), tab, sT), B)) + __ldg(rk + slot);
     Es[p] = E;
-    if (idx) idx[p] = __ldg(cidx + i);
+    if (idx) idx[p] = __ldg(cidx + slot);
   }
 }
 
@@ -351,6 +348,18 @@ static int sort_bits_override() {  // A/B override GF_SORT_BITS in [10, 17], rea
     const char *f = getenv("GF_SORT_BITS");
     const int b = f ? atoi(f) : 0;
     return (b >= 10 && b <= 17) ? b : 0;
+  }();
+  return v;
+}
+
+// Energy slices of the whole-grid scatter: 2 (gpurun_out/r02al, C3 17 M step: 1 slice 2.680 ms (DRAM
+// 162 MB read + 371 MB written by the scatter: partial sectors evicted), 2 slices 2.612, 3 2.616, 4 2.626:
+// each slice re-samples the batch).  GF_SCATTER_SLICES overrides (A/B), read once per process.
+static int scatter_slices() {
+  static const int v = [] {
+    const char *f = getenv("GF_SCATTER_SLICES");
+    const int k = f ? atoi(f) : 2;
+    return (k >= 1 && k <= 16) ? k : 2;
   }();
   return v;
 }
@@ -401,7 +410,7 @@ static SortBins sort_bins(uint32_t n, double lo, double hi) {
                             fhi ? state_threshold(hi) : 1ull << 63});
 }
 
-// Words of the count / cursor arrays (12 x 2^17 bins, + the compact-list counter of band grids).
+// Words of the count / cursor arrays (12 x 2^17 bins).
 size_t sort_hist_words(uint64_t) { return ((size_t)kMats << 17) + 1; }
 
 cudaError_t launch_sort_zero(uint32_t n, const SortScratch &S, cudaStream_t st) {
@@ -425,15 +434,15 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
   const SortBins B = S.counted ? whole_bins(sort_bits(n)) : sort_bins(n, band_lo, band_hi);
   const int bins = kMats << B.nbl;  // a multiple of kScanBlk for nbl >= 10
   const TixSpec T = (tix && !src_E) ? *tix : TixSpec{};  // (bin edges bound sampled energies only)
-  // band grids take sampled lookups only (abi.cu): the compact-list path; its counter sits behind the bins
+  // band grids take sampled lookups only (abi.cu): the compact-list path
   const bool band = B.slo != 0ull || B.shi != (1ull << 63);
   if (band && (src_E || S.counted)) return cudaErrorInvalidValue;
   if (!S.counted) {
-    if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * (bins + (band ? 1 : 0)), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
     const unsigned gc = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
     if (band)
       sort_count_band<<<gc, kSampTpb, 0, st>>>(first, n, seed, thr, S.counts, B, reinterpret_cast<uint64_t *>(S.Et),
-                                                S.rk, want_idx ? S.idxt : nullptr, S.counts + bins);
+                                                S.rk, want_idx ? S.idxt : nullptr, S.segcnt);
     else
       sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, B, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -443,15 +452,22 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
   scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, S.counts, B, T);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (band) {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned gs = std::min(nblk(n, 256), (unsigned)sms * 8u);
-    sort_scatter_band<<<gs, 256, 0, st>>>(reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, thr, S.cursor, S.Es,
-                                          want_idx ? S.idx : nullptr, B, S.mstart);
+    const uint32_t nseg = (uint32_t)(((uint64_t)n + kSeg - 1) / kSeg);
+    sort_scatter_band<<<nblk((long long)nseg * 32, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, S.segcnt, nseg, thr, S.cursor, S.Es,
+        want_idx ? S.idx : nullptr, B);
   } else {
-    sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(
-        first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B);
+    // sampled batches scatter in energy slices (one launch each, the others' lookups skipped on the LCG
+    // state): a slice's destinations (1/K of the sorted array) stay in L2 until its sectors are complete,
+    // instead of partial sectors going to DRAM read-modify-write
+    const int K = src_E ? 1 : scatter_slices();
+    for (int k = 0; k < K; k++) {
+      const unsigned long long lo = k ? state_threshold((double)k / K) : 0ull;
+      const unsigned long long hi = k + 1 < K ? state_threshold((double)(k + 1) / K) : 1ull << 63;
+      sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(
+          first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B, lo, hi - lo);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
   }
   return cudaGetLastError();
 }

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t 
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
                                                   SortBins B, unsigned long long *__restrict__ flag) {
   __shared__ SampleSmem Q;
+  pdl_trigger();
   stage_sampler(Q, thr, first, seed, !src_E);
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
@@ -123,6 +124,8 @@ __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t 
 __global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restrict__ counts,
                                                        uint32_t *__restrict__ cursor, uint32_t *__restrict__ btot) {
   __shared__ uint32_t wsum[32];
+  pdl_trigger();
+  pdl_wait();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int b = blockIdx.x * kScanBlk + tid;
   const uint32_t c = counts[b];
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ curs
                                                      uint32_t *__restrict__ mstart, const uint32_t *__restrict__ counts,
                                                      SortBins B, TixSpec T) {
   __shared__ uint32_t s_off;
+  pdl_trigger();
+  pdl_wait();
   const int nb_log2 = B.nbl;
   const int nblocks = (kMats << nb_log2) / kScanBlk;
   if (threadIdx.x < 32) {
@@ -215,7 +220,9 @@ __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_
                                                     double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B,
                                                     unsigned long long slo, unsigned long long sspan) {
   __shared__ SampleSmem Q;
+  pdl_trigger();
   stage_sampler(Q, thr, first, seed, !src_E);
+  pdl_wait();  // (the cursors come from scan_add)
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
   const int cnt = (int)min((uint64_t)kRun, n - t0);
@@ -263,53 +270,61 @@ __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint
                                                        const double *__restrict__ thr, uint32_t *__restrict__ counts,
                                                        SortBins B, uint64_t *__restrict__ cs,
                                                        uint32_t *__restrict__ rk, uint32_t *__restrict__ cidx,
-                                                       uint32_t *__restrict__ segcnt) {
+                                                       uint32_t *__restrict__ segcnt, unsigned long long a_stride,
+                                                       unsigned long long c_stride) {
   __shared__ unsigned long long q[kSampTpb * kQStride];
   __shared__ uint8_t qp[kSampTpb * kRun];
   __shared__ uint32_t wpre[kSampTpb / 32][32];
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t g = blockIdx.x * (kSampTpb / 32) + w;  // segment
-  const uint64_t w0 = (uint64_t)g * kSeg;
-  if (w0 >= n) return;  // (warp-uniform)
+  const uint32_t nwarps = gridDim.x * (kSampTpb / 32);
+  const uint32_t nseg = (uint32_t)(((uint64_t)n + kSeg - 1) / kSeg);
+  uint32_t g = blockIdx.x * (kSampTpb / 32) + w;  // this warp's first segment; then every nwarps-th
+  if (g >= nseg) return;  // (warp-uniform)
   const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
   const uint8_t *tab = tb + kMatTabOff;
   const unsigned long long *sT = reinterpret_cast<const unsigned long long *>(thr) + kMats;
-  const uint64_t base = lcg_skip_warp(seed, 2ull * (first + w0));
   const ulonglong2 m = __ldg(reinterpret_cast<const ulonglong2 *>(tb + kOffMapOff) + lane);  // 32 lane steps
-  const uint64_t t0 = w0 + (uint64_t)lane * kRun;
+  // the lane's start state for its 16 lookups of segment g; the next segment's is one affine map away
+  uint64_t s0 = (m.x * lcg_skip_warp(seed, 2ull * (first + (uint64_t)g * kSeg)) + m.y) & kLcgMask;
   const unsigned long long span = B.shi - B.slo;
-  uint32_t cnt = 0;
   unsigned long long *row = q + threadIdx.x * kQStride;
   uint8_t *prow = qp + threadIdx.x * kRun;
-  sample_run((m.x * base + m.y) & kLcgMask, B, [&](int r, uint64_t s1) {
-    if (t0 + r < n && s1 - B.slo < span) {
-      row[cnt] = s1;
-      prow[cnt] = (uint8_t)r;
-      cnt++;
+  for (; g < nseg; g += nwarps) {
+    const uint64_t w0 = (uint64_t)g * kSeg, t0 = w0 + (uint64_t)lane * kRun;
+    uint32_t cnt = 0;
+    sample_run(s0, B, [&](int r, uint64_t s1) {
+      if (t0 + r < n && s1 - B.slo < span) {
+        row[cnt] = s1;
+        prow[cnt] = (uint8_t)r;
+        cnt++;
+      }
+    });
+    s0 = (a_stride * s0 + c_stride) & kLcgMask;
+    uint32_t x = cnt;  // warp prefix of the queue lengths
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-  });
-  uint32_t x = cnt;  // warp prefix of the queue lengths
+    wpre[w][lane] = x - cnt;
+    const uint32_t wn = __shfl_sync(0xffffffffu, x, 31);
+    if (lane == 0) segcnt[g] = wn;
+    __syncwarp();
+    for (uint32_t j = lane; j < wn; j += 32) {
+      int o = 0;  // the lane whose queue holds entry j: max{o : wpre[o] <= j}
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  wpre[w][lane] = x - cnt;
-  const uint32_t wn = __shfl_sync(0xffffffffu, x, 31);
-  if (lane == 0) segcnt[g] = wn;
-  __syncwarp();
-  for (uint32_t j = lane; j < wn; j += 32) {
-    int o = 0;  // the lane whose queue holds entry j: max{o : wpre[o] <= j}
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1)
-      if (wpre[w][o + step] <= j) o += step;
-    const uint32_t k = j - wpre[w][o];
-    const int src = w * 32 + o;
-    const uint64_t s1 = q[src * kQStride + k];
-    const size_t slot = (size_t)w0 + j;
-    rk[slot] = atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), tab, sT), B), 1u);
-    cs[slot] = s1;
-    if (cidx) cidx[slot] = (uint32_t)(w0 + (uint64_t)o * kRun + qp[src * kRun + k]);
+      for (int step = 16; step > 0; step >>= 1)
+        if (wpre[w][o + step] <= j) o += step;
+      const uint32_t k = j - wpre[w][o];
+      const int src = w * 32 + o;
+      const uint64_t s1 = q[src * kQStride + k];
+      const size_t slot = (size_t)w0 + j;
+      rk[slot] = atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), tab, sT), B), 1u);
+      cs[slot] = s1;
+      if (cidx) cidx[slot] = (uint32_t)(w0 + (uint64_t)o * kRun + qp[src * kRun + k]);
+    }
+    __syncwarp();  // (the queue rows are refilled by the next segment)
   }
 }
 
@@ -322,6 +337,8 @@ __global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restr
                                                          uint32_t *__restrict__ idx, SortBins B) {
   const int lane = threadIdx.x & 31;
   const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  pdl_trigger();
+  pdl_wait();
   if (g >= nseg) return;
   const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
   const uint8_t *tab = tb + kMatTabOff;
@@ -440,22 +457,31 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
   if (!S.counted) {
     if ((e = cudaMemsetAsync(S.counts, 0, sizeof(uint32_t) * bins, st)) != cudaSuccess) return e;
     const unsigned gc = nblk(((long long)n + kRun - 1) / kRun, kSampTpb);
-    if (band)
-      sort_count_band<<<gc, kSampTpb, 0, st>>>(first, n, seed, thr, S.counts, B, reinterpret_cast<uint64_t *>(S.Et),
-                                                S.rk, want_idx ? S.idxt : nullptr, S.segcnt);
-    else
+    if (band) {  // persistent: the resident warps walk the segments, stepping their states by one map
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_count_band, kSampTpb, 0);
+      const unsigned gb = std::min(gc, (unsigned)(sms * std::max(per_sm, 1)));
+      uint64_t A, C;
+      lcg_skip_map(2ull * kSeg * gb * (kSampTpb / 32), A, C);
+      sort_count_band<<<gb, kSampTpb, 0, st>>>(first, n, seed, thr, S.counts, B, reinterpret_cast<uint64_t *>(S.Et),
+                                                S.rk, want_idx ? S.idxt : nullptr, S.segcnt, A, C);
+    } else {
       sort_count<<<gc, kSampTpb, 0, st>>>(first, n, seed, src_E, src_mat, thr, S.counts, B, flag);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, S.counts, B, T);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_pdl(scan_local, bins / kScanBlk, kScanBlk, 0, st, S.counts, S.cursor, S.btot)) != cudaSuccess) return e;
+  if ((e = launch_pdl(scan_add, bins / kScanBlk, kScanBlk, 0, st, S.cursor, S.btot, S.mstart, S.counts, B, T)) !=
+      cudaSuccess)
+    return e;
   if (band) {
     const uint32_t nseg = (uint32_t)(((uint64_t)n + kSeg - 1) / kSeg);
-    sort_scatter_band<<<nblk((long long)nseg * 32, 256), 256, 0, st>>>(
-        reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, S.segcnt, nseg, thr, S.cursor, S.Es,
-        want_idx ? S.idx : nullptr, B);
+    if ((e = launch_pdl(sort_scatter_band, nblk((long long)nseg * 32, 256), 256, 0, st,
+                        reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, S.segcnt, nseg, thr, S.cursor, S.Es,
+                        want_idx ? S.idx : nullptr, B)) != cudaSuccess)
+      return e;
   } else {
     // sampled batches scatter in energy slices (one launch each, the others' lookups skipped on the LCG
     // state): a slice's destinations (1/K of the sorted array) stay in L2 until its sectors are complete,
@@ -464,9 +490,10 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
     for (int k = 0; k < K; k++) {
       const unsigned long long lo = k ? state_threshold((double)k / K) : 0ull;
       const unsigned long long hi = k + 1 < K ? state_threshold((double)(k + 1) / K) : 1ull << 63;
-      sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(
-          first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B, lo, hi - lo);
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      if ((e = launch_pdl(sort_scatter, nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st, first, n,
+                          seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B, lo, hi - lo)) !=
+          cudaSuccess)
+        return e;
     }
   }
   return cudaGetLastError();

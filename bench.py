@@ -47,6 +47,9 @@ CONFIGS = {
     # NEXT-2 energy-band sharding: XSBench XL on the unionized grid, whose index grid (355 x 84.8 M
     # entries) fits no GPU whole; 8 energy bands, rank r of N serves bands r, r + N, ...
     "C7": ("xs", 355, 1, 17_000_000, "XSBench XL 355x238847, unionized grid in 8 energy bands, 17M event lookups (NEXT-2)"),
+    # NEXT-2 XXL (R-XXL: 2.1 x XL = 501,579 gridpoints per nuclide): the unionized grid in 16 bands (a band's
+    # index grid needs < 65,536 points per nuclide); one GPU runs them in turn
+    "C8": ("xs", 355, 1, 17_000_000, "XSBench XXL 355x501579, unionized grid in 16 energy bands, 17M event lookups (NEXT-2)"),
     # NEXT-4: page-rank propagation step (HeCBench page-rank), 2^24 nodes, out-degree 16
     "P1": ("pr", 1 << 24, 16, 0, "page-rank propagation step, 2^24 nodes, average out-degree 16 (NEXT-4)"),
     # NEXT-4: AMGmk relax kernel: one Jacobi sweep, 27-point Laplacian on 256^3
@@ -75,7 +78,9 @@ PAPER_KEY = {"C1": "xs_event_small", "C2": "xs_event_small", "C3": "xs_event_lar
 #   C5: RSBench flops counted from the oracle's arithmetic: 55.4 nuclides x (51 per
 #   nuclide + 9.09 poles x 85 per pole) + 0.5% Abrarov evaluations ~ 49,000 (transcendental = 1 flop);
 #   C5D0 (0 K): 55.4 x (51 + 9.09 x 43 per pole: sqrt, two textbook complex divisions, 3 products) ~ 24,500.
-ALG = {"C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
+GRIDPOINTS = {"C6": 238847, "C7": 238847, "C8": 501579}  # (else 11,303)
+BANDS = {"C7": 8, "C8": 16}
+ALG = {"C8": (6517, 1551), "C1": (7187, 434), "C2": (1887, 434), "C3": (6517, 1551), "C4": (6203, 1551), "C5": (0, 49000),
        "C3N": (0, 1551), "C5D0": (0, 24500), "C6": (6203, 1551), "C7": (6517, 1551), "H2": (1887, 434), "H3": (6517, 1551), "H5": (0, 49000)}
 
 
@@ -194,8 +199,8 @@ def cpu_baseline(cfg_name, seconds=12.0):
     bench, n_iso, gt, n, _ = CONFIGS[cfg_name]
     threads = len(os.sched_getaffinity(0))
     if bench == "xs":
-        o = O.XSOracle(n_iso, 238847 if cfg_name in ("C6", "C7") else 11303, O.NUCLIDE if cfg_name == "C7" else gt,
-                       bins=10000)  # (C7: the nuclide grid gives the unionized grid's results; its IG is 120 GB)
+        o = O.XSOracle(n_iso, GRIDPOINTS.get(cfg_name, 11303), O.NUCLIDE if cfg_name in BANDS else gt,
+                       bins=10000)  # (C7 / C8: the nuclide grid gives the unionized grid's results; its IG is 120 GB+)
     else:
         o = O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1)
     k = 20_000
@@ -273,7 +278,7 @@ def run_reference(args, rank, world):
                 "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
-    o = (O.XSOracle(n_iso, 238847 if cfg_name in ("C6", "C7") else 11303, O.NUCLIDE if cfg_name == "C7" else gt,
+    o = (O.XSOracle(n_iso, GRIDPOINTS.get(cfg_name, 11303), O.NUCLIDE if cfg_name in BANDS else gt,
                     bins=10000) if bench == "xs"
          else O.RSOracle(n_iso, 1000, 100, 4, doppler=0 if cfg_name == "C5D0" else 1))
     t = time.perf_counter()
@@ -306,18 +311,19 @@ def run_reference(args, rank, world):
 
 
 def bench_bands(args, rank, world, dev, gf, torch, dist, C):
-    """C7: every rank builds, in turn, the band replicas of its bands (r, r + N, ... of W = 8; grid build
-    untimed), and runs the full event batch through each -- the sort keeps the band's lookups.  A step
-    is one batch through all of the rank's bands; value = 17 M / max-over-ranks step time."""
+    """C7 / C8: every rank builds, in turn, the band replicas of its bands (r, r + N, ... of W = 8 / 16;
+    grid build untimed), and runs the full event batch through each -- the sort keeps the band's lookups.
+    A step is one batch through all of the rank's bands; value = 17 M / max-over-ranks step time."""
     from paper_2306_11686_b200 import dist as gdist
-    W, n = 8, CONFIGS["C7"][3]
+    cfg = args.config
+    W, n, n_gp = BANDS[cfg], CONFIGS[cfg][3], GRIDPOINTS[cfg]
     mine = list(range(rank, W, world))
     st = torch.cuda.current_stream()
     vsum = torch.zeros(1, dtype=torch.int64, device=dev)
     per_band, raws, builds = [], 0, 0.0
     for b in mine:
         t0 = time.perf_counter()
-        grid = gf.Grid(gf.Params.xsbench(355, 238847, gf.UNIONIZED, n_bands=W, band=b), device=dev)
+        grid = gf.Grid(gf.Params.xsbench(355, n_gp, gf.UNIONIZED, n_bands=W, band=b), device=dev)
         builds += time.perf_counter() - t0
         sc = torch.empty(grid.scratch_bytes(n, gf.SORT_LOCALITY), dtype=torch.uint8, device=dev)
         ts = []
@@ -344,7 +350,7 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
     if rank == 0:
         peaks = load_peaks()
         look_s = step_ms * 1e-3
-        roof = {"bound": "alu", "kernel": "sort + idx_prep + xs_lookup_group<unionized> per band",
+        roof = {"bound": "alu", "kernel": "band sort + xs_lookup_tile<unionized> per band",
                 "achieved": 1551 * n / look_s / 1e12, "peak": peaks["fp64_dadd_ops_per_s"] / 1e12,
                 "unit": "TFLOP/s", "traffic": None,
                 "note": "1551 fp64 flops/lookup x 17 M lookups / summed band step time (each band re-samples and "
@@ -354,11 +360,11 @@ def bench_bands(args, rank, world, dev, gf, torch, dist, C):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (LCG-generated grids and lookups, seeds 42 / 1070)",
-                "config": {"workload": f"C7: {CONFIGS['C7'][4]}", "n_lookups": n, "bands": W,
+                "config": {"workload": f"{cfg}: {CONFIGS[cfg][4]}", "n_lookups": n, "bands": W,
                            "bands_per_rank": len(mine), "band_ms": per_band,
                            "parallelism": f"energy bands over {world} rank(s), 1 int64 all-reduce"},
                 "roofline": roof, "cpu_baseline": None, "e2e": None,
-                "gpu_launches": args.steps * len(mine) * 6, "hash": gf.verify(int(rv.item())),
+                "gpu_launches": args.steps * len(mine) * 5, "hash": gf.verify(int(rv.item())),
                 "raw": int(rv.item()), "grid_build_s": builds}
         print(json.dumps(line), flush=True)
 
@@ -581,8 +587,8 @@ def main():
             dist.init_process_group(backend)
         dist.barrier()
     dev = torch.device("cuda", local)
-    if args.config in ("C7", "P1", "A1"):
-        if args.config == "C7":
+    if args.config in ("C7", "C8", "P1", "A1"):
+        if args.config in BANDS:
             bench_bands(args, rank, world, dev, gf, torch, dist, C)
         elif args.config == "P1":
             bench_pagerank(args, rank, world, dev, gf, torch, dist)

@@ -689,6 +689,20 @@ def test_band_tile_path_per_lookup(gf, torch, W, b):
     check_bands_one(gf, torch, o, g, W, b, 5_000_000, 400_000)
 
 
+def test_C8_xxl_bands_sum(gf, torch):
+    """NEXT-2 XXL (R-XXL: 355 x 501,579 gridpoints, 2.1 x XL): the 16 energy-band replicas of the unionized
+    grid (16 so that a band's index grid stays below 65,536 points per nuclide) together reproduce the
+    oracle's XXL raw sum (tests/golden/make_golden.py --xxl, on its hash grid: identical intervals)."""
+    gold = golden()
+    n, W, raw = 17_000_000, 16, 0
+    for b in range(W):
+        g = gf.Grid(gf.Params.xsbench(355, 501579, gf.UNIONIZED, n_bands=W, band=b))
+        raw += g.lookup_batch(0, n)
+        del g
+        torch.cuda.empty_cache()
+    assert raw == gold["C8"]["raw"]
+
+
 def check_bands_one(gf, torch, o, g, W, b, first, n):
     raw_o, m_o = o.lookup_batch(first, n, want_macro=True)
     E = np.array([O.sample(first + i)[0] for i in range(n)])

@@ -21,6 +21,11 @@ for gt in (gf.NUCLIDE, gf.UNIONIZED, gf.HASH):
     for k in kernels:
         g.set_kernel(k)
         out.append((gt, k, g.lookup_batch(0, n, want_macro=True)[0]))
+    if gt == gf.UNIONIZED:  # per-tile union indices from the sort's scan (TixSpec) + the tile kernel's PREP path
+        g.set_kernel("tile")
+        g.set_prep_min(0)
+        out.append((gt, "tile-prep", g.lookup_batch(0, n, want_macro=True)[0]))
+        g.set_prep_min(8 << 20)
     g.set_kernel("auto")
     out.append((gt, "unsorted", g.lookup_batch(0, n, sort=False)))
     out.append((gt, "energies", g.lookup_energies(E.cuda(), M.cuda())[0]))
@@ -33,6 +38,9 @@ for gt in (gf.NUCLIDE, gf.UNIONIZED, gf.HASH):
 for band in (0, 3):
     gb = gf.Grid(gf.Params.xsbench(68, 11303, gf.UNIONIZED, n_bands=4, band=band))
     out.append(("band", band, gb.lookup_batch(0, n)))
+    gb.set_kernel("tile")
+    gb.set_prep_min(0)
+    out.append(("band-tile", band, gb.lookup_batch(0, n, want_macro=True)[0]))
     del gb
 r = gf.Grid(gf.Params.rsbench(68))
 out.append(("rs", "sorted", r.lookup_batch(0, 20000)))

@@ -249,9 +249,11 @@ static void kernel_choice(XsDev &X) {
   X.tile_min = kTileMinN;
   if (const char *m = getenv("GF_XS_TILE_MIN")) X.tile_min = (uint32_t)strtoul(m, nullptr, 10);
   X.group_min = kGroupMinN;
-  if (X.grid_type == GF_GRID_HASH && X.n_gp > 65536) {
-    // XL hash grids (C6): a tile's runs outgrow the staging buffers for the sparse materials, and the
-    // group kernel wins from 2 M lookups (gpurun_out/r02ak, C6 17 M: group 15.7 ms, tile 17.4, thread 19.9)
+  if ((X.grid_type == GF_GRID_HASH && X.n_gp > 65536) || (X.grid_type == GF_GRID_UNIONIZED && X.n_gp > 262144)) {
+    // XL hash and XXL unionized grids: a tile's runs (~n_gp x the tile's energy width per nuclide)
+    // outgrow the staging buffers, and the group kernel wins from 2 M lookups (gpurun_out/r02ak, C6 XL
+    // hash 17 M: group 15.7 ms, tile 17.4, thread 19.9; r02ax, C8 XXL in 16 bands: group 25.1 ms, tile 48.7;
+    // the XL unionized bands of C7 stay on the tile kernel: 12.1 vs group 15.0 ms)
     X.tile_min = 0xFFFFFFFFu;
     X.group_min = kTileMinN;
   }

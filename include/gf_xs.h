@@ -202,6 +202,19 @@ gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint
                                 double *macro_out, uint64_t *vsum, void *scratch, size_t scratch_bytes,
                                 gf_stream_t stream);
 
+/* Streaming form of the host-I/O call, for back-to-back batches: caller energies and materials from
+ * (pinned) HOST memory, everything ENQUEUED on `stream` with no host wait -- the copies of E[n] (8 B) and
+ * mat[n] (1 B) into the scratch, the sorted lookup (flags must be GF_SORT_LOCALITY: the whole-batch sort,
+ * PAPER.md:1408 event lookups), and the raw sum ADDED to the DEVICE accumulator *d_vsum.  A caller
+ * alternating two scratch buffers on two streams overlaps batch k+1's copies with batch k's lookups.
+ * The host arrays must stay unchanged and the scratch unused until the stream has passed this call.
+ * Scratch: gf_xs_batch_bytes_whole(g, n, GF_SORT_LOCALITY | GF_HOST_IO).  No per-lookup outputs.
+ * Invalid inputs (mat > 11, non-finite E) set bit 63 of *d_vsum (gf_xs_verify: GF_E_INVAL).  Not for
+ * band grids (their batches are sampled).  n < 2^32. */
+gf_status gf_xs_lookup_energies_async(const gf_xs_grid *g, const double *E_host, const uint8_t *mat_host, uint64_t n,
+                                      uint32_t flags, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                                      gf_stream_t stream);
+
 /* NEXT-1: HISTORY-BASED lookups, PAPER.md:1408 ("event-based lookup and
  * history-based lookup").  Particles with GLOBAL indices [first_particle, first_particle + n_particles)
  * each run `lookups_per_particle` (L, 34 in XSBench / RSBench) DEPENDENT lookups; the readings

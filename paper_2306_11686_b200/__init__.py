@@ -89,6 +89,7 @@ def lib():
             "gf_xs_lookup_batch": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_lookup_batch_ev": (i32, [vp, u64, u64, u64, C.c_uint32, vp, vp, vp, sz, vp, vp]),
             "gf_xs_lookup_energies": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, vp, sz, vp]),
+            "gf_xs_lookup_energies_async": (i32, [vp, vp, vp, u64, C.c_uint32, vp, vp, sz, vp]),
             "gf_xs_history_bytes": (i32, [vp, u64, C.c_uint32, P(sz)]),
             "gf_xs_history_batch": (i32, [vp, u64, u64, i32, u64, C.c_uint32, vp, vp, vp, sz, vp]),
             "gf_xs_verify": (i32, [u64, u64, P(u64)]),
@@ -354,6 +355,24 @@ class Grid:
         if raw < 0:  # bit 63: the invalid-input flag
             raise GFError(1, "invalid caller inputs: material id > 11 or non-finite energy")
         return (raw, macro) if want_macro else raw
+
+    def lookup_energies_async(self, E, mat, d_vsum, scratch, stream=None):
+        """gf_xs_lookup_energies_async: pinned HOST E (float64 [n]) and mat (uint8 [n]) copied and looked up
+        (sorted) on `stream` without waiting; the raw sum is ADDED to the device int64 tensor d_vsum[0].
+        `scratch`: a device uint8 tensor of scratch_bytes(n, SORT_LOCALITY | HOST_IO, whole=True) bytes,
+        not reused until the stream has passed this call (alternate two for back-to-back batches)."""
+        torch = self.torch
+        self._check_states(E, mat, None, False)
+        if E.is_cuda or mat.is_cuda:
+            raise ValueError("E and mat must be host tensors (pinned for asynchronous copies)")
+        if d_vsum.device != self.device or d_vsum.dtype != torch.int64:
+            raise ValueError("d_vsum must be an int64 tensor on the grid's device")
+        if scratch.device != self.device or scratch.dtype != torch.uint8:
+            raise ValueError("scratch must be a uint8 tensor on the grid's device")
+        _check(lib().gf_xs_lookup_energies_async(self.h, C.c_void_p(E.data_ptr()), C.c_void_p(mat.data_ptr()),
+                                                 E.numel(), SORT_LOCALITY, C.c_void_p(d_vsum.data_ptr()),
+                                                 C.c_void_p(scratch.data_ptr()), scratch.numel(),
+                                                 _stream_ptr(torch, stream)))
 
     # ----------------------------------------------------------------- history mode (NEXT-1)
     HIST_MODES = {"direct": 0, "waves": HIST_WAVES, "sorted": HIST_WAVES | SORT_LOCALITY}

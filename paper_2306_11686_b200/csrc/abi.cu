@@ -799,6 +799,32 @@ gf_status gf_xs_lookup_energies(const gf_xs_grid *g, const double *E, const uint
   }
 }
 
+gf_status gf_xs_lookup_energies_async(const gf_xs_grid *g, const double *E_host, const uint8_t *mat_host, uint64_t n,
+                                      uint32_t flags, uint64_t *d_vsum, void *scratch, size_t scratch_bytes,
+                                      gf_stream_t stream) {
+  if (!g || !d_vsum || (n && (!E_host || !mat_host))) return fail(GF_E_INVAL, "grid, d_vsum, E or mat is NULL");
+  if (flags != GF_SORT_LOCALITY) return fail(GF_E_INVAL, "flags must be GF_SORT_LOCALITY");
+  if (n >= (1ull << 32)) return fail(GF_E_INVAL, "n %llu >= 2^32", (unsigned long long)n);
+  if (g->p.bench == GF_XSBENCH && g->p.n_bands > 1) return fail(GF_E_INVAL, "band grids take sampled lookups only");
+  if (n == 0) return GF_OK;
+  DeviceGuard dg(g->device);
+  BatchLayout B;
+  plan_batch(g, n, GF_SORT_LOCALITY | GF_HOST_IO, false, true, B, true);  // the whole-batch slot
+  const SlotLayout &L = B.full;
+  if (!scratch || scratch_bytes < L.bytes)
+    return fail(GF_E_NOMEM, "scratch %zu B < required %zu B", scratch_bytes, L.bytes);
+  char *sc = static_cast<char *>(scratch);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double *dE = reinterpret_cast<double *>(sc + L.h_E);
+  uint8_t *dmat = reinterpret_cast<uint8_t *>(sc + L.h_mat);
+  GF_CUDA(cudaMemcpyAsync(dE, E_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  GF_CUDA(cudaMemcpyAsync(dmat, mat_host, n, cudaMemcpyHostToDevice, st));
+  const cudaError_t ce = launch_lookup(g, 0, (uint32_t)n, 0, dE, dmat, true, slot_sort(sc, L), nullptr,
+                                       reinterpret_cast<unsigned long long *>(d_vsum), st, nullptr);
+  if (ce != cudaSuccess) return fail(GF_E_CUDA, "lookup launch: %s", cudaGetErrorString(ce));
+  return GF_OK;
+}
+
 // ------------------------------------------------------------------------------------------ history (NEXT-1)
 // Waves scratch: per particle the LCG state (8 B), this wave's E (8 B) and material (1 B), the
 // feedback byte of the previous wave, then one sort slot for n_particles lookups.

@@ -327,6 +327,35 @@ def test_energies_api_device_and_host(gf, torch, grid_type):
     assert raw_h == raw_o and np.array_equal(m_h.numpy(), m_o)
 
 
+def test_energies_async_stream(gf, torch):
+    """gf_xs_lookup_energies_async: back-to-back batches from pinned host memory on two streams (one scratch
+    each) add the oracle's raw sum to the device accumulators; invalid inputs set bit 63; a short scratch
+    is refused."""
+    o, g = make_pair(gf, 68, 11303, O.UNIONIZED)
+    rng = np.random.default_rng(5)
+    n = 300_000
+    E = rng.random(n)
+    mat = rng.integers(0, 12, n).astype(np.uint8)
+    raw_o, _ = o.lookup_energies(E, mat.astype(np.int32))
+    Eh, mh = torch.from_numpy(E).pin_memory(), torch.from_numpy(mat).pin_memory()
+    need = g.scratch_bytes(n, gf.SORT_LOCALITY | gf.HOST_IO, whole=True)
+    scr = [torch.empty(need, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    dv = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for k in range(4):
+        with torch.cuda.stream(sts[k % 2]):
+            g.lookup_energies_async(Eh, mh, dv[k % 2:k % 2 + 1], scr[k % 2], stream=sts[k % 2])
+    torch.cuda.synchronize()
+    assert dv.tolist() == [2 * raw_o, 2 * raw_o]
+    mh[7] = 12
+    d1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    g.lookup_energies_async(Eh, mh, d1, scr[0])
+    torch.cuda.synchronize()
+    assert int(d1.item()) < 0  # bit 63: the invalid-input flag
+    with pytest.raises(gf.GFError):
+        g.lookup_energies_async(Eh, mh, d1, scr[0][:1024])
+
+
 @pytest.mark.parametrize("grid_type", [1, 2])
 def test_sorted_groups_at_interval_edges(gf, torch, grid_type):
     """Sorted lookups share record pairs and (hash grid) the interval shortcut R-SHORT, which takes

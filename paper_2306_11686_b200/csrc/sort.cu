@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t 
                                                   const double *__restrict__ thr, uint32_t *__restrict__ counts,
                                                   SortBins B, unsigned long long *__restrict__ flag) {
   __shared__ SampleSmem Q;
-  pdl_trigger();
   stage_sampler(Q, thr, first, seed, !src_E);
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
@@ -124,8 +123,6 @@ __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t 
 __global__ void __launch_bounds__(kScanBlk) scan_local(const uint32_t *__restrict__ counts,
                                                        uint32_t *__restrict__ cursor, uint32_t *__restrict__ btot) {
   __shared__ uint32_t wsum[32];
-  pdl_trigger();
-  pdl_wait();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int b = blockIdx.x * kScanBlk + tid;
   const uint32_t c = counts[b];
@@ -186,8 +183,6 @@ __global__ void __launch_bounds__(kScanBlk) scan_add(uint32_t *__restrict__ curs
                                                      uint32_t *__restrict__ mstart, const uint32_t *__restrict__ counts,
                                                      SortBins B, TixSpec T) {
   __shared__ uint32_t s_off;
-  pdl_trigger();
-  pdl_wait();
   const int nb_log2 = B.nbl;
   const int nblocks = (kMats << nb_log2) / kScanBlk;
   if (threadIdx.x < 32) {
@@ -220,9 +215,7 @@ __global__ void __launch_bounds__(kSampTpb) sort_scatter(uint64_t first, uint32_
                                                     double *__restrict__ Es, uint32_t *__restrict__ idx, SortBins B,
                                                     unsigned long long slo, unsigned long long sspan) {
   __shared__ SampleSmem Q;
-  pdl_trigger();
   stage_sampler(Q, thr, first, seed, !src_E);
-  pdl_wait();  // (the cursors come from scan_add)
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
   const int cnt = (int)min((uint64_t)kRun, n - t0);
@@ -275,7 +268,6 @@ __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint
   __shared__ unsigned long long q[kSampTpb * kQStride];
   __shared__ uint8_t qp[kSampTpb * kRun];
   __shared__ uint32_t wpre[kSampTpb / 32][32];
-  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (kSampTpb / 32);
   const uint32_t nseg = (uint32_t)(((uint64_t)n + kSeg - 1) / kSeg);
@@ -337,8 +329,6 @@ __global__ void __launch_bounds__(256) sort_scatter_band(const uint64_t *__restr
                                                          uint32_t *__restrict__ idx, SortBins B) {
   const int lane = threadIdx.x & 31;
   const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  pdl_trigger();
-  pdl_wait();
   if (g >= nseg) return;
   const unsigned char *tb = reinterpret_cast<const unsigned char *>(thr);
   const uint8_t *tab = tb + kMatTabOff;
@@ -472,16 +462,16 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  if ((e = launch_pdl(scan_local, bins / kScanBlk, kScanBlk, 0, st, S.counts, S.cursor, S.btot)) != cudaSuccess) return e;
-  if ((e = launch_pdl(scan_add, bins / kScanBlk, kScanBlk, 0, st, S.cursor, S.btot, S.mstart, S.counts, B, T)) !=
-      cudaSuccess)
-    return e;
+  scan_local<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.counts, S.cursor, S.btot);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  scan_add<<<bins / kScanBlk, kScanBlk, 0, st>>>(S.cursor, S.btot, S.mstart, S.counts, B, T);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (band) {
     const uint32_t nseg = (uint32_t)(((uint64_t)n + kSeg - 1) / kSeg);
-    if ((e = launch_pdl(sort_scatter_band, nblk((long long)nseg * 32, 256), 256, 0, st,
-                        reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, S.segcnt, nseg, thr, S.cursor, S.Es,
-                        want_idx ? S.idx : nullptr, B)) != cudaSuccess)
-      return e;
+    sort_scatter_band<<<nblk((long long)nseg * 32, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint64_t *>(S.Et), S.rk, S.idxt, S.segcnt, nseg, thr, S.cursor, S.Es,
+        want_idx ? S.idx : nullptr, B);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   } else {
     // sampled batches scatter in energy slices (one launch each, the others' lookups skipped on the LCG
     // state): a slice's destinations (1/K of the sorted array) stay in L2 until its sectors are complete,
@@ -490,10 +480,9 @@ cudaError_t launch_locality_sort(uint64_t first, uint32_t n, uint64_t seed, cons
     for (int k = 0; k < K; k++) {
       const unsigned long long lo = k ? state_threshold((double)k / K) : 0ull;
       const unsigned long long hi = k + 1 < K ? state_threshold((double)(k + 1) / K) : 1ull << 63;
-      if ((e = launch_pdl(sort_scatter, nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st, first, n,
-                          seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B, lo, hi - lo)) !=
-          cudaSuccess)
-        return e;
+      sort_scatter<<<nblk(((long long)n + kRun - 1) / kRun, kSampTpb), kSampTpb, 0, st>>>(
+          first, n, seed, src_E, src_mat, thr, S.cursor, S.Es, want_idx ? S.idx : nullptr, B, lo, hi - lo);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
   }
   return cudaGetLastError();

@@ -413,7 +413,6 @@ static cudaError_t launch_gt(const XsDev &X, uint64_t first, uint32_t n, uint64_
     // caller energies (possibly clamped into a material's last bin) take tile_prep's exact tile extremes
     const bool tix = GT == GF_GRID_UNIONIZED && kern == kKernTile && n >= X.prep_min && !src_E && !GF_TILE_PREP;
     const TixSpec T{reinterpret_cast<uint2 *>(S.us), X.ubin, X.U, X.n_union};
-    if ((e = cudaMemsetAsync(S.work, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;  // (tile kernels' counter)
     if ((e = launch_locality_sort(first, n, seed, src_E, src_mat, X.thr, S, out.any(), vsum, st, X.band_lo, X.band_hi,
                                   tix ? &T : nullptr)) != cudaSuccess)
       return e;

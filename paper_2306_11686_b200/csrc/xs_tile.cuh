@@ -471,10 +471,8 @@ __global__ void __launch_bounds__(kTileTpb, GF_TILE_MINB)
   __shared__ uint32_t ms[kMats + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   TileSmem &S = reinterpret_cast<TileSmem *>(smem + tile_table_bytes(X.total))[warp];
-  const XsTables T = stage_xs_tables<true, GT == kGridNB>(X, smem);  // (grid data: before the sort completes)
-  pdl_wait();  // the sorted batch, its material starts and tile indices, the work counter
   if (threadIdx.x <= kMats) ms[threadIdx.x] = __ldg(mstart + threadIdx.x);
-  __syncthreads();
+  const XsTables T = stage_xs_tables<true, GT == kGridNB>(X, smem);  // (its __syncthreads publishes ms)
   n = min(n, ms[kMats]);  // lookups kept by the sort (band grids keep their band's)
   uint32_t vacc = 0;
   const uint32_t ntiles = (n + 32 * kL - 1) / (32 * kL);
@@ -690,9 +688,9 @@ static cudaError_t launch_tile_p(const XsDev &X, uint32_t n, const SortScratch &
     idx_prep<GT><<<nblk(((long long)n + 3) / 4, 256), 256, 0, st>>>(X, n, S.Es, S.mstart, S.us);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  // (the work counter was zeroed before the sort: launch_gt; no memset between the sort and this kernel)
-  return launch_pdl(xs_lookup_tile<GT, FAST, PREP>, grid, kTileTpb, smem, st, X, n, (const double *)S.Es,
-                    (const uint32_t *)S.us, (const uint32_t *)S.idx, (const uint32_t *)S.mstart, out, vsum, S.work);
+  if ((e = cudaMemsetAsync(S.work, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
+  xs_lookup_tile<GT, FAST, PREP><<<grid, kTileTpb, smem, st>>>(X, n, S.Es, S.us, S.idx, S.mstart, out, vsum, S.work);
+  return cudaGetLastError();
 }
 
 template <int GT, bool FAST>

@@ -202,20 +202,27 @@ __device__ __forceinline__ void rs_macro(const RsDev &R, const Tables &T, double
     int w = (int)(E / spacing);
     if (w == nw) w--;
     w = w < 0 ? 0 : (w > nw - 1 ? nw - 1 : w);
+    // Phase factors fac_l = e^{-2 i phi_l}, phi_l = p - atan(a_l / b_l), p = K0RS_l sqrt(E) (R-RSPHI: l = 1:
+    // (a, b) = (-p, 1); l = 2: (3p, 3 - p^2); l = 3: (p (15 - p^2), 15 - 6 p^2)).  Since
+    // e^{2 i atan(a / b)} = (b + i a)^2 / (a^2 + b^2) for any real a, b not both 0 (a b < 0 or b < 0 only
+    // shifts the angle by a multiple of pi, which doubling removes), fac_l = e^{-2 i p} (b + i a)^2 / (a^2 + b^2):
+    // one sincos per l and no atan (R-UNIQ: within rounding of the oracle's atan + sincos).
     cplx fac[4];
 #pragma unroll
     for (int l = 0; l < 4; l++) {
-      double phi = __ldg(R.K0RS + nuc * 4 + l) * sqrtE;
-      if (l == 1)
-        phi -= -atan(phi);
-      else if (l == 2)
-        phi -= atan(3.0 * phi / (3.0 - phi * phi));
-      else if (l == 3)
-        phi -= atan(phi * (15.0 - phi * phi) / (15.0 - 6.0 * phi * phi));
-      phi *= 2.0;
+      const double p = __ldg(R.K0RS + nuc * 4 + l) * sqrtE;
       double sn, cs;
-      sincos(phi, &sn, &cs);
-      fac[l] = {cs, -sn};
+      sincos(2.0 * p, &sn, &cs);
+      if (l == 0) {
+        fac[l] = {cs, -sn};
+      } else {
+        const double p2 = p * p;
+        const double a = l == 1 ? -p : (l == 2 ? 3.0 * p : p * (15.0 - p2));
+        const double b = l == 1 ? 1.0 : (l == 2 ? 3.0 - p2 : 15.0 - 6.0 * p2);
+        const double rd = 1.0 / (a * a + b * b);
+        const double rr = (b * b - a * a) * rd, ri = 2.0 * a * b * rd;
+        fac[l] = {cs * rr + sn * ri, cs * ri - sn * rr};  // (cs - i sn) (rr + i ri)
+      }
     }
     const double2 *wp = reinterpret_cast<const double2 *>(R.win + w0 + w);
     const double2 W0 = __ldg(wp), W1 = __ldg(wp + 1);

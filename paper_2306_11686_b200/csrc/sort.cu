@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(kSampTpb) sort_count(uint64_t first, uint32_t 
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
   if (t0 >= n) return;
   if (!src_E) {
+    const int rem = (int)min((uint64_t)kRun, n - t0);
     sample_run(thread_start(thr, Q), B, [&](int r, uint64_t s1) {
-      if (t0 + r < n)
-        atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
+      if (r < rem) atomicAdd(counts + bin_of(lcg_unit(s1), pick_material_tab(lcg_next(s1), Q.tab, Q.sT), B), 1u);
     });
     return;
   }
@@ -284,9 +284,10 @@ __global__ void __launch_bounds__(kSampTpb) sort_count_band(uint64_t first, uint
   uint8_t *prow = qp + threadIdx.x * kRun;
   for (; g < nseg; g += nwarps) {
     const uint64_t w0 = (uint64_t)g * kSeg, t0 = w0 + (uint64_t)lane * kRun;
+    const int rem = t0 < n ? (int)min((uint64_t)kRun, n - t0) : 0;  // (32-bit compares in the unrolled loop)
     uint32_t cnt = 0;
     sample_run(s0, B, [&](int r, uint64_t s1) {
-      if (t0 + r < n && s1 - B.slo < span) {
+      if (r < rem && s1 - B.slo < span) {
         row[cnt] = s1;
         prow[cnt] = (uint8_t)r;
         cnt++;

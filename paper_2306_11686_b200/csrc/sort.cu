@@ -6,10 +6,11 @@
 // integer hash, outputs scattered back through idx).
 // Counting sort: sort_count (sample, one global atomic per lookup on its bin), a two-kernel scan (which
 // also writes the material starts and, for unionized tile batches, the per-tile union indices),
-// sort_scatter (sample again, atomic cursor, store E and the lookup position).  Sampling is
-// index-addressed (lookup i draws from fast_forward(seed, 2i)): a thread skips once and steps through
-// 16 consecutive lookups as two interleaved LCG chains; the material roll is decided on the integer LCG
-// state (pick_material_tab, exact).
+// sort_scatter (sample again, atomic cursor, store E and the lookup position; sampled batches in two
+// energy slices so that each slice's destinations stay in L2).  Sampling is index-addressed (lookup i
+// draws from fast_forward(seed, 2i)): warp 0 composes the CTA's skip (lcg_skip_warp), each thread starts
+// from it through an offset map and steps through 16 consecutive lookups as two interleaved LCG chains;
+// the material roll is decided on the integer LCG state (pick_material_tab, exact).
 // A band grid (NEXT-2) keeps only lookups with band_lo <= E < band_hi: its count pass (sort_count_band)
 // samples the whole batch once, keeps the ~n/W in-band LCG states in a compact list (per-warp segments)
 // with each one's rank inside its bin (the count atomic's return value), and the scatter
